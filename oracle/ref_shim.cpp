@@ -1,0 +1,238 @@
+// ref_shim.cpp -- TEST INFRASTRUCTURE ONLY (builds oracle/_ref/libssam_ref.so).
+//
+// A thin extern "C" wrapper over the UNMODIFIED reference, compiled straight
+// from /root/reference/proj/{include,src} by oracle/Makefile with the
+// reference's own Release flags (-O3 -DNDEBUG -fopenmp, proj/CMakeLists.txt:5-11).
+// No reference source is copied into this repo; this file only adapts the
+// reference's C++ templates to plain pointers so Python can drive them.
+//
+// Exposed:
+//   * the reference's CPU SSAM path (ssam::conv2d/stencil2d/stencil3d,
+//     proj/include/ssam/kernels.hpp:189,231,283) -- the CPU baseline that
+//     bench.py --impl reference times, and the source of OpCounters truth;
+//   * the reference oracle (proj/include/ssam/oracle.hpp:44-116) and input
+//     generators (grid.hpp:52-66, filter.hpp:41-47) -- used to pin
+//     oracle/ssam_oracle.c through tests/golden/.
+//
+// Status codes mirror the C ABI: 0 ok, 1 std::invalid_argument,
+// 2 std::length_error, 9 anything else.
+
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "ssam/filter.hpp"
+#include "ssam/grid.hpp"
+#include "ssam/kernels.hpp"
+#include "ssam/oracle.hpp"
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+using namespace ssam;
+
+namespace {
+
+enum { F32 = 0, F64 = 1, I64 = 2 };
+
+template <class Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::length_error&) {
+    return 2;
+  } catch (const std::invalid_argument&) {
+    return 1;
+  } catch (...) {
+    return 9;
+  }
+}
+
+KernelConfig make_cfg(int p, int b, int boundary, int lane_count, int threads) {
+  KernelConfig cfg;
+  cfg.p = p;
+  cfg.b = b;
+  cfg.boundary = boundary ? Boundary::replicate : Boundary::zero;
+  cfg.lane_count = lane_count;
+  cfg.threads = threads;
+  return cfg;
+}
+
+void put_counters(const OpCounters& c, std::uint64_t* out) {
+  if (!out) return;
+  out[0] = c.mads;
+  out[1] = c.shuffles;
+  out[2] = c.broadcast_reads;
+  out[3] = c.global_loads;
+  out[4] = c.global_stores;
+}
+
+template <class T>
+Stencil<T> make_stencil(int dims, int order, const int* offsets, const void* coeffs, int ntaps) {
+  Stencil<T> st;
+  st.name = "abi";
+  st.dims = dims;
+  st.order = order;
+  const T* c = static_cast<const T*>(coeffs);
+  for (int j = 0; j < ntaps; ++j)
+    st.taps.push_back({{offsets[3 * j], offsets[3 * j + 1], offsets[3 * j + 2]}, c[j]});
+  return st;
+}
+
+template <class T>
+int conv2d_t(const void* in, int w, int h, const void* wts, int m, int n, const KernelConfig& cfg,
+             void* out, std::uint64_t* counters, bool naive) {
+  return guarded([&] {
+    Grid2D<T> g(w, h);
+    std::memcpy(g.data.data(), in, sizeof(T) * g.data.size());
+    const T* wp = static_cast<const T*>(wts);
+    Filter2D<T> f(m, n, std::vector<T>(wp, wp + static_cast<std::size_t>(m) * n));
+    OpCounters c;
+    Grid2D<T> r = naive ? oracle::conv2d_naive(g, f, cfg.boundary) : conv2d(g, f, cfg, &c);
+    std::memcpy(out, r.data.data(), sizeof(T) * r.data.size());
+    put_counters(c, counters);
+  });
+}
+
+template <class T>
+int stencil2d_t(const void* in, int w, int h, const Stencil<T>& st, const KernelConfig& cfg,
+                int iters, void* out, std::uint64_t* counters, bool naive) {
+  return guarded([&] {
+    Grid2D<T> g(w, h);
+    std::memcpy(g.data.data(), in, sizeof(T) * g.data.size());
+    OpCounters c;
+    Grid2D<T> r = naive ? oracle::stencil2d_naive(g, st, iters) : stencil2d(g, st, cfg, iters, &c);
+    std::memcpy(out, r.data.data(), sizeof(T) * r.data.size());
+    put_counters(c, counters);
+  });
+}
+
+template <class T>
+int stencil3d_t(const void* in, int nx, int ny, int nz, const Stencil<T>& st,
+                const KernelConfig& cfg, int iters, void* out, std::uint64_t* counters,
+                bool naive) {
+  return guarded([&] {
+    Grid3D<T> g(nx, ny, nz);
+    std::memcpy(g.data.data(), in, sizeof(T) * g.data.size());
+    OpCounters c;
+    Grid3D<T> r = naive ? oracle::stencil3d_naive(g, st, iters) : stencil3d(g, st, cfg, iters, &c);
+    std::memcpy(out, r.data.data(), sizeof(T) * r.data.size());
+    put_counters(c, counters);
+  });
+}
+
+}  // namespace
+
+extern "C" {
+
+int ssam_ref_max_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
+
+// naive != 0 runs oracle::conv2d_naive instead of the SSAM simulator.
+int ssam_ref_conv2d(int dtype, const void* in, int w, int h, const void* wts, int m, int n,
+                    int p, int b, int boundary, int lane_count, int threads, void* out,
+                    std::uint64_t* counters, int naive) {
+  const KernelConfig cfg = make_cfg(p, b, boundary, lane_count, threads);
+  switch (dtype) {
+    case F32: return conv2d_t<float>(in, w, h, wts, m, n, cfg, out, counters, naive);
+    case F64: return conv2d_t<double>(in, w, h, wts, m, n, cfg, out, counters, naive);
+    case I64: return conv2d_t<long long>(in, w, h, wts, m, n, cfg, out, counters, naive);
+  }
+  return 9;
+}
+
+int ssam_ref_stencil2d(int dtype, const void* in, int w, int h, int dims, int order,
+                       const int* offsets, const void* coeffs, int ntaps, int p, int b,
+                       int lane_count, int threads, int iters, void* out,
+                       std::uint64_t* counters, int naive) {
+  const KernelConfig cfg = make_cfg(p, b, 0, lane_count, threads);
+  switch (dtype) {
+    case F32:
+      return stencil2d_t<float>(in, w, h, make_stencil<float>(dims, order, offsets, coeffs, ntaps),
+                                cfg, iters, out, counters, naive);
+    case F64:
+      return stencil2d_t<double>(in, w, h,
+                                 make_stencil<double>(dims, order, offsets, coeffs, ntaps), cfg,
+                                 iters, out, counters, naive);
+    case I64:
+      return stencil2d_t<long long>(
+          in, w, h, make_stencil<long long>(dims, order, offsets, coeffs, ntaps), cfg, iters, out,
+          counters, naive);
+  }
+  return 9;
+}
+
+int ssam_ref_stencil3d(int dtype, const void* in, int nx, int ny, int nz, int dims, int order,
+                       const int* offsets, const void* coeffs, int ntaps, int p, int b,
+                       int lane_count, int threads, int iters, void* out,
+                       std::uint64_t* counters, int naive) {
+  const KernelConfig cfg = make_cfg(p, b, 0, lane_count, threads);
+  switch (dtype) {
+    case F32:
+      return stencil3d_t<float>(in, nx, ny, nz,
+                                make_stencil<float>(dims, order, offsets, coeffs, ntaps), cfg,
+                                iters, out, counters, naive);
+    case F64:
+      return stencil3d_t<double>(in, nx, ny, nz,
+                                 make_stencil<double>(dims, order, offsets, coeffs, ntaps), cfg,
+                                 iters, out, counters, naive);
+    case I64:
+      return stencil3d_t<long long>(in, nx, ny, nz,
+                                    make_stencil<long long>(dims, order, offsets, coeffs, ntaps),
+                                    cfg, iters, out, counters, naive);
+  }
+  return 9;
+}
+
+// random_grid2d<T>(count, 1, seed) draws the same stream as random_grid3d.
+int ssam_ref_random_grid(int dtype, void* out, int count, std::uint64_t seed) {
+  return guarded([&] {
+    switch (dtype) {
+      case F32: { auto g = random_grid2d<float>(count, 1, seed); std::memcpy(out, g.data.data(), 4ul * count); break; }
+      case F64: { auto g = random_grid2d<double>(count, 1, seed); std::memcpy(out, g.data.data(), 8ul * count); break; }
+      default: { auto g = random_grid2d<long long>(count, 1, seed); std::memcpy(out, g.data.data(), 8ul * count); break; }
+    }
+  });
+}
+
+int ssam_ref_random_filter(int dtype, void* out, int m, int n, std::uint64_t seed) {
+  return guarded([&] {
+    const std::size_t cnt = static_cast<std::size_t>(m) * n;
+    switch (dtype) {
+      case F32: { auto f = random_filter<float>(m, n, seed); std::memcpy(out, f.w.data(), 4 * cnt); break; }
+      case F64: { auto f = random_filter<double>(m, n, seed); std::memcpy(out, f.w.data(), 8 * cnt); break; }
+      default: { auto f = random_filter<long long>(m, n, seed); std::memcpy(out, f.w.data(), 8 * cnt); break; }
+    }
+  });
+}
+
+int ssam_ref_benchmark_stencil(const char* name, int* dims, int* order, int* fpp, int* offsets,
+                               double* coeffs, int cap) {
+  try {
+    Stencil<double> st = make_benchmark_stencil(name);
+    if (static_cast<int>(st.taps.size()) > cap) return -2;
+    for (std::size_t j = 0; j < st.taps.size(); ++j) {
+      offsets[3 * j] = st.taps[j].offset[0];
+      offsets[3 * j + 1] = st.taps[j].offset[1];
+      offsets[3 * j + 2] = st.taps[j].offset[2];
+      coeffs[j] = st.taps[j].coeff;
+    }
+    *dims = st.dims;
+    *order = st.order;
+    *fpp = st.fpp;
+    return static_cast<int>(st.taps.size());
+  } catch (...) {
+    return -1;
+  }
+}
+
+}  // extern "C"
