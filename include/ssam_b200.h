@@ -1,0 +1,193 @@
+/*
+ * ssam_b200.h -- C ABI of the B200-native SSAM engine (libssam_b200.so).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * has no FFI layer: its boundary is the three C++ templates of
+ * proj/include/ssam/kernels.hpp (relative to /root/reference):
+ *
+ *   Grid2D<T> conv2d   (const Grid2D<T>&, const Filter2D<T>&, const KernelConfig&,
+ *                       OpCounters* = nullptr);                            // kernels.hpp:189
+ *   Grid2D<T> stencil2d(const Grid2D<T>&, const Stencil<T>&, const KernelConfig&,
+ *                       int iters, OpCounters* = nullptr);                 // kernels.hpp:231
+ *   Grid3D<T> stencil3d(const Grid3D<T>&, const Stencil<T>&, const KernelConfig&,
+ *                       int iters, OpCounters* = nullptr);                 // kernels.hpp:283
+ *
+ * with T in {float, double, long long} (proj/tools/ssam_cli.cpp:241-243).
+ * Each entry point below replaces one of them; include/ssam_b200/kernels.hpp
+ * re-exposes the exact C++ signatures on top of this ABI and re-raises the
+ * reference's exception types from the status codes.
+ *
+ * Plain pointers and sizes only: no C++, torch or reference types cross it.
+ * Grids are dense, row-major, x fastest: 2D data[y*W + x] (grid.hpp:11-28),
+ * 3D data[(z*ny + y)*nx + x] (grid.hpp:30-49).
+ *
+ * Every call runs on the GPU.  There is no CPU fallback: without a CUDA
+ * device the compute entry points return SSAM_ERR_NO_DEVICE.  Validation
+ * happens first and needs no device, so the error contract is testable on
+ * any host.
+ */
+#ifndef SSAM_B200_H
+#define SSAM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSAM_B200_ABI_VERSION 1
+
+/* Element type of a call: float, double, long long (int64). */
+typedef enum { SSAM_DTYPE_F32 = 0, SSAM_DTYPE_F64 = 1, SSAM_DTYPE_I64 = 2 } ssam_dtype;
+
+/* ssam::Boundary (filter.hpp:15): zero padding or clamp-replicate. */
+typedef enum { SSAM_BOUNDARY_ZERO = 0, SSAM_BOUNDARY_REPLICATE = 1 } ssam_boundary;
+
+typedef enum {
+  SSAM_OK = 0,
+  SSAM_ERR_INVALID_ARGUMENT = 1, /* the reference throws std::invalid_argument */
+  SSAM_ERR_LENGTH = 2,           /* the reference throws std::length_error (C > 255) */
+  SSAM_ERR_CUDA = 3,             /* CUDA runtime failure; see ssam_b200_last_error() */
+  SSAM_ERR_NO_DEVICE = 4,        /* no usable CUDA device */
+  SSAM_ERR_OUT_OF_MEMORY = 5     /* device allocation failed */
+} ssam_status;
+
+/* ssam::KernelConfig (filter.hpp:117-139).  Validated exactly like
+ * KernelConfig::check(); after validation p, b, lane_count and threads are
+ * tuning hints only -- results never depend on them. */
+typedef struct {
+  int p;          /* outputs per lane per tile (reference default 4) */
+  int b;          /* threads per block (reference default 128) */
+  int boundary;   /* ssam_boundary; conv2d only */
+  int lane_count; /* simulated warp width, power of two in [2, 64] */
+  int threads;    /* CPU worker threads in the reference; ignored */
+} ssam_kernel_config;
+
+/* ssam::OpCounters (warp.hpp:12-28).  Filled with exactly what the
+ * reference's simulator counts for the same call (closed forms), and
+ * ACCUMULATED into (+=), as kernels.hpp:50-54 does. */
+typedef struct {
+  uint64_t mads;
+  uint64_t shuffles;
+  uint64_t broadcast_reads;
+  uint64_t global_loads;
+  uint64_t global_stores;
+} ssam_op_counters;
+
+/* ssam::Stencil<T> (filter.hpp:52-68): ntaps (dx, dy, dz) offsets and their
+ * coefficients, stored as elements of the call's dtype. */
+typedef struct {
+  int dims;           /* 2 or 3 */
+  int order;          /* k: largest |offset| component */
+  int ntaps;
+  const int* offsets; /* 3 * ntaps ints: dx, dy, dz per tap */
+  const void* coeffs; /* ntaps elements of the call's dtype */
+} ssam_stencil;
+
+/* ---- library ------------------------------------------------------------ */
+int ssam_b200_abi_version(void);
+/* Message for the last non-OK status on the calling thread ("" if none). */
+const char* ssam_b200_last_error(void);
+/* Number of CUDA devices (0 when none is usable). */
+int ssam_b200_device_count(void);
+/* KernelConfig defaults: p=4, b=128, zero boundary, lane_count=32, threads=0. */
+void ssam_b200_default_config(ssam_kernel_config* cfg);
+/* Kernel launches issued by this process so far (evidence for benchmarks). */
+uint64_t ssam_b200_launch_count(void);
+
+/* ---- host-grid entry points (replace kernels.hpp:189 / :231 / :283) -----
+ * in/out are host pointers of width*height (or nx*ny*nz) elements; they may
+ * not alias.  Synchronous.  Pinned host memory gives full-speed copies. */
+int ssam_b200_conv2d(int dtype, const void* in, int width, int height, const void* weights, int m,
+                     int n, const ssam_kernel_config* cfg, void* out, ssam_op_counters* counters);
+
+int ssam_b200_stencil2d(int dtype, const void* in, int width, int height, const ssam_stencil* st,
+                        const ssam_kernel_config* cfg, int iters, void* out,
+                        ssam_op_counters* counters);
+
+int ssam_b200_stencil3d(int dtype, const void* in, int nx, int ny, int nz, const ssam_stencil* st,
+                        const ssam_kernel_config* cfg, int iters, void* out,
+                        ssam_op_counters* counters);
+
+/* Validation only (no device needed): the status the call above would
+ * return for these arguments before touching the GPU. */
+int ssam_b200_check_conv2d(int width, int height, int m, int n, const ssam_kernel_config* cfg);
+int ssam_b200_check_stencil2d(int width, int height, const ssam_stencil* st,
+                              const ssam_kernel_config* cfg, int iters);
+int ssam_b200_check_stencil3d(int nx, int ny, int nz, const ssam_stencil* st,
+                              const ssam_kernel_config* cfg, int iters);
+
+/* Closed-form OpCounters of the reference simulator for a call (no device). */
+int ssam_b200_counters_conv2d(int width, int height, int m, int n, const ssam_kernel_config* cfg,
+                              ssam_op_counters* counters);
+int ssam_b200_counters_stencil2d(int width, int height, const ssam_stencil* st,
+                                 const ssam_kernel_config* cfg, int iters,
+                                 ssam_op_counters* counters);
+int ssam_b200_counters_stencil3d(int nx, int ny, int nz, const ssam_stencil* st,
+                                 const ssam_kernel_config* cfg, int iters,
+                                 ssam_op_counters* counters);
+
+/* ---- benchmark catalog (proj/src/stencil_catalog.cpp:81-127) ------------- */
+int ssam_b200_benchmark_count(void);
+const char* ssam_b200_benchmark_name(int index);
+/* make_benchmark_stencil(name): writes up to cap taps (offsets 3*cap ints,
+ * coeffs cap doubles); returns the tap count, or -1 for an unknown name
+ * (the reference throws std::invalid_argument). */
+int ssam_b200_benchmark_stencil(const char* name, int* dims, int* order, int* fpp, int* offsets,
+                                double* coeffs, int cap);
+
+/* ---- device-resident entry points (benchmarks, multi-GPU) -----------------
+ * Pointers are device memory of the current device, 16-byte alignment and
+ * width % (16/sizeof(T)) == 0 give the vectorised path.  stream is a
+ * cudaStream_t (NULL = legacy default stream).  Asynchronous. */
+
+/* conv2d over output rows [y_begin, y_end) of a width x height buffer.  A
+ * row slab of a larger image passes only the rows it holds: rows outside
+ * the buffer are the image boundary (zero or replicate). */
+int ssam_b200_conv2d_device(int dtype, const void* d_in, void* d_out, int width, int height,
+                            int y_begin, int y_end, const void* h_weights, int m, int n,
+                            int boundary, void* stream);
+
+/* One Jacobi sweep over output rows [y_begin, y_end) ∩ [k, height-k).  Only
+ * interior cells are written: d_out's ring must already equal d_in's. */
+int ssam_b200_stencil2d_sweep(int dtype, const void* d_in, void* d_out, int width, int height,
+                              int y_begin, int y_end, const ssam_stencil* st, void* stream);
+
+/* tb fused sweeps (temporal blocking) over the whole grid; returns
+ * SSAM_ERR_INVALID_ARGUMENT if no fused kernel exists for this case. */
+int ssam_b200_stencil2d_tb(int dtype, const void* d_in, void* d_out, int width, int height,
+                           const ssam_stencil* st, int tb, void* stream);
+/* Deepest fused temporal block available for (dtype, stencil); 1 = none. */
+int ssam_b200_stencil2d_tb_max(int dtype, const ssam_stencil* st);
+
+/* One Jacobi sweep over output planes [z_begin, z_end) ∩ [k, nz-k) of an
+ * nx x ny x nz buffer (a z-slab with ghost planes passes local indices). */
+int ssam_b200_stencil3d_sweep(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
+                              int z_begin, int z_end, const ssam_stencil* st, void* stream);
+
+/* iters sweeps with ping-pong buffers.  d_a holds the input; d_b is scratch
+ * of the same size whose ring this call initialises.  *d_result receives
+ * d_a or d_b, whichever holds the final generation.  tb: temporal block
+ * depth (0 = automatic, 1 = none). */
+int ssam_b200_stencil2d_run(int dtype, void* d_a, void* d_b, int width, int height,
+                            const ssam_stencil* st, int iters, int tb, void* stream,
+                            void** d_result);
+int ssam_b200_stencil3d_run(int dtype, void* d_a, void* d_b, int nx, int ny, int nz,
+                            const ssam_stencil* st, int iters, void* stream, void** d_result);
+
+/* Device SplitMix64 fill, bit-identical to the reference's random_grid2d/3d:
+ * element i receives stream draw (first + i) of seed (rng.hpp, grid.hpp:52-66). */
+int ssam_b200_fill_random(int dtype, void* d_out, size_t count, uint64_t seed, uint64_t first,
+                          void* stream);
+
+/* max_i |a_i - b_i| / max(1, |b_i|) and max |a_i - b_i| (acceptance.cpp:35-44),
+ * reduced on the device; synchronises the stream. */
+int ssam_b200_max_rel_err(int dtype, const void* d_a, const void* d_b, size_t count,
+                          double* max_rel, double* max_abs, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SSAM_B200_H */

@@ -1,0 +1,74 @@
+// common.cuh -- device helpers shared by the SSAM engines (sm_100a).
+//
+// The SSAM execution model of arXiv 1907.06154 maps onto Blackwell as:
+//   * a warp is the systolic array: 32 lanes, each owning Q consecutive grid
+//     columns (Q*sizeof(T) = 16 B, one 128-bit load per row per lane);
+//   * the register file is the cache: each lane keeps a sliding window of
+//     rows (2D) or planes (3D) of its Q columns in registers;
+//   * partial sums travel lane to lane with __shfl_up_sync -- a one-column
+//     shift is Q-1 register renames plus ONE shuffle of the lane's last
+//     element, so the shuffle cost per output is 1/Q of the paper's;
+//   * there is no shared-memory round trip per tap.
+// Reference semantics: proj/include/ssam/plan.hpp:103-159 (PE update rule
+// s <- ctrl(r (x) x) (+) shift(s)), warp.hpp:59-77 (shfl_up keeps low lanes).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ssam_b200 {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Q columns per lane so one row segment is one 16-byte access per lane.
+template <class T> struct Lanes { static constexpr int Q = 16 / sizeof(T); };
+
+// 16-byte aligned Q-vector used for 128-bit global loads/stores.
+template <class T, int Q>
+struct alignas(sizeof(T) * Q) VecT {
+  T v[Q];
+};
+
+template <class T>
+__device__ __forceinline__ T fma_t(T a, T b, T c) { return a * b + c; }
+template <>
+__device__ __forceinline__ float fma_t<float>(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+template <>
+__device__ __forceinline__ double fma_t<double>(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+template <class T>
+__device__ __forceinline__ T shfl_up(T v, int d) { return __shfl_up_sync(kFull, v, d); }
+
+// Shift a lane-distributed row of 32*Q values one column toward higher x:
+// element i takes element i-1.  Lane 0's first element keeps its own value
+// (shfl_up semantics, warp.hpp:59-77); it only ever feeds invalid outputs.
+template <class T, int Q>
+__device__ __forceinline__ void shift1(T (&a)[Q]) {
+  const T top = shfl_up(a[Q - 1], 1);
+#pragma unroll
+  for (int q = Q - 1; q > 0; --q) a[q] = a[q - 1];
+  a[0] = top;
+}
+
+// Read-only 128-bit load through the non-coherent path.
+template <class T, int Q>
+__device__ __forceinline__ void ld_vec(const T* __restrict__ p, T (&out)[Q]) {
+  static_assert(sizeof(T) * Q == 16, "128-bit vectors only");
+  const int4 r = __ldg(reinterpret_cast<const int4*>(p));
+  VecT<T, Q> v;
+  memcpy(&v, &r, sizeof(r));
+#pragma unroll
+  for (int q = 0; q < Q; ++q) out[q] = v.v[q];
+}
+
+template <class T, int Q>
+__device__ __forceinline__ void st_vec(T* p, const T (&in)[Q]) {
+  VecT<T, Q> v;
+#pragma unroll
+  for (int q = 0; q < Q; ++q) v.v[q] = in[q];
+  *reinterpret_cast<VecT<T, Q>*>(p) = v;
+}
+
+__device__ __forceinline__ int clampi(int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); }
+
+}  // namespace ssam_b200

@@ -1,0 +1,86 @@
+// internal.hpp -- host-side contracts between the C ABI (abi.cpp) and the
+// kernel launchers (*.cu).  No reference or torch types; plain pointers.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+namespace ssam_b200 {
+
+enum class Shape2D { other, star };
+enum class Shape3D { other, star, box, poisson };
+
+struct Tap {
+  int dx, dy, dz;
+};
+
+// Tap-set classification used for kernel selection; the coefficients are
+// always the caller's (any values), only the offset set is matched.
+Shape2D classify2d(const std::vector<Tap>& taps, int order);
+Shape3D classify3d(const std::vector<Tap>& taps, int order);
+
+template <class T>
+struct StencilDesc {
+  int dims = 2;
+  int order = 0;
+  std::vector<Tap> taps;
+  std::vector<T> coeffs;
+};
+
+// ---- conv2d: out = sum_{s,t} in(x+ax-s, y+ay-t) * w[s*n+t] -----------------
+// d_in/d_out device pointers (distinct); h_w host pointer to m*n weights.
+// Output rows [y_begin, y_end); rows outside [0, H) are the image boundary.
+template <class T>
+cudaError_t conv2d_device(const T* d_in, T* d_out, int W, int H, int y_begin, int y_end,
+                          const T* h_w, int m, int n, int boundary, cudaStream_t s);
+
+// ---- one Jacobi sweep (2D), interior cells only ---------------------------
+// Writes next(x,y) for k <= x < W-k and y in [y_begin, y_end) ∩ [k, H-k).
+// Ring cells of d_out are left untouched (callers keep them equal to the
+// input ring).
+template <class T>
+cudaError_t stencil2d_sweep(const T* d_in, T* d_out, int W, int H, int y_begin, int y_end,
+                            const StencilDesc<T>& st, cudaStream_t s);
+
+// Tb fused sweeps (temporal blocking).  Returns cudaErrorNotSupported when no
+// fused kernel exists for this stencil/dtype/Tb (the caller then sweeps).
+template <class T>
+cudaError_t stencil2d_tb(const T* d_in, T* d_out, int W, int H, const StencilDesc<T>& st, int tb,
+                         cudaStream_t s);
+int stencil2d_tb_max(int dtype, int order, bool star);
+
+// ---- one Jacobi sweep (3D) over output planes [z_begin, z_end) ------------
+// Plane indices are global to the (nz-plane) buffer; the ring test uses
+// ring_lo/ring_hi for z so a slab can place the true domain faces.
+template <class T>
+cudaError_t stencil3d_sweep(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin,
+                            int z_end, const StencilDesc<T>& st, cudaStream_t s);
+
+// ---- direct-gather kernels (generic path: any order / tap set) -------------
+// Bit-faithful to the oracle's summation order (double accumulation for FP,
+// no FMA contraction), used where no SSAM specialisation applies.
+template <class T>
+cudaError_t conv2d_direct(const T* d_in, T* d_out, int W, int H, const T* h_w, int m, int n,
+                          int boundary, cudaStream_t s);
+template <class T>
+cudaError_t stencil2d_direct(const T* d_in, T* d_out, int W, int H, int y_begin, int y_end,
+                             const StencilDesc<T>& st, cudaStream_t s);
+template <class T>
+cudaError_t stencil3d_direct(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin,
+                             int z_end, const StencilDesc<T>& st, cudaStream_t s);
+
+// ---- utilities --------------------------------------------------------------
+cudaError_t fill_random(int dtype, void* d, std::size_t count, std::uint64_t seed,
+                        std::uint64_t first, cudaStream_t s);
+// max |a-b| / max(1,|b|) and max |a-b| over count elements, into host doubles.
+cudaError_t max_rel_err(int dtype, const void* d_a, const void* d_b, std::size_t count,
+                        double* h_rel, double* h_abs, cudaStream_t s);
+
+// How many launches of our kernels the last host call issued (bench evidence).
+void note_launch();
+std::uint64_t launches();
+
+}  // namespace ssam_b200

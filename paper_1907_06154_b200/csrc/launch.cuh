@@ -1,0 +1,140 @@
+// launch.cuh -- host-side launch planning for the SSAM engines.
+#pragma once
+
+#include <algorithm>
+#include <cstring>
+
+#include "engine2d.cuh"
+#include "engine3d.cuh"
+#include "internal.hpp"
+
+namespace ssam_b200 {
+
+constexpr int kSMs = 148;          // B200: 2 dies x 74 SMs
+constexpr int kWarpsPerBlock = 4;  // 128-thread blocks
+
+// Lane plan for an M-column footprint with Q columns per lane (engine2d.cuh):
+//   R = (M-1)/2, L = M-1-R; E extra shifts make the landing offset G a
+//   multiple of Q; A (>= L, multiple of Q) is the left halo the warp loads;
+//   V = 32Q - G - A outputs per warp row, a multiple of Q.
+struct LanePlan {
+  int e, G, A, V;
+};
+inline LanePlan plan_lanes(int M, int Q) {
+  const int R = (M - 1) / 2, L = M - 1 - R;
+  LanePlan lp;
+  lp.e = (Q - R % Q) % Q;
+  lp.G = R + lp.e;
+  lp.A = (L + Q - 1) / Q * Q;
+  lp.V = 32 * Q - lp.G - lp.A;
+  return lp;
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(p) & 15u) == 0; }
+
+// Rows streamed per warp: enough warps for ~2 waves of ~24 resident warps/SM,
+// but long enough that the NR-1 prologue rows stay a small overhead.
+inline int pick_seg(int rows, int nstrips, int nr) {
+  const long long target_warps = static_cast<long long>(kSMs) * 48;
+  long long segs = (target_warps + nstrips - 1) / nstrips;
+  segs = std::max<long long>(1, std::min<long long>(segs, rows));
+  int seg = static_cast<int>((rows + segs - 1) / segs);
+  seg = std::max(seg, std::min(rows, 8 * nr));
+  return std::max(seg, 1);
+}
+
+template <class T>
+struct Engine2DArgs {
+  const T* in;
+  T* out;
+  int W, H;
+  int M, NR;
+  const T* coef;  // host, [M][NR]
+  int bmode, ring;
+  int y_begin, y_end;
+};
+
+template <class T, int Q, int NR, int MC, class Mask, int PF, int CAP>
+cudaError_t launch_ssam2d(const Engine2DArgs<T>& a, cudaStream_t s) {
+  static_assert(MC == 0 || MC * NR <= CAP, "coefficient capacity");
+  if (a.M * NR > CAP || a.NR != NR || (MC > 0 && a.M != MC)) return cudaErrorInvalidValue;
+  if (a.y_end <= a.y_begin) return cudaSuccess;
+  Ssam2DParams<T, CAP> p;
+  std::memset(&p, 0, sizeof(p));
+  p.in = a.in;
+  p.out = a.out;
+  p.W = a.W;
+  p.H = a.H;
+  p.M = a.M;
+  const LanePlan lp = plan_lanes(a.M, Q);
+  p.e = lp.e;
+  p.G = lp.G;
+  p.A = lp.A;
+  p.V = lp.V;
+  p.nstrips = (a.W + lp.V - 1) / lp.V;
+  const int rows = a.y_end - a.y_begin;
+  p.seg = pick_seg(rows, p.nstrips, NR);
+  p.y_begin = a.y_begin;
+  p.y_end = a.y_end;
+  p.bmode = a.bmode;
+  p.ring = a.ring;
+  p.vec_ok = (a.W % Q == 0) && aligned16(a.in) && aligned16(a.out);
+  std::memcpy(p.coef, a.coef, sizeof(T) * a.M * NR);
+  const dim3 grid((p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock, (rows + p.seg - 1) / p.seg);
+  ssam2d_kernel<T, Q, NR, MC, Mask, PF, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+template <class T>
+struct Engine3DArgs {
+  const T* in;
+  T* out;
+  int nx, ny, nz;
+  int K;
+  const T* coef;  // host, [(2K+1)^3] as coef[(l*M + j)*M + t]
+  int z_begin, z_end;
+};
+
+template <class T, int Q, int K, class Mask, int RY, int PFZ, int CAP>
+cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
+  constexpr int M = 2 * K + 1;
+  static_assert(M * M * M <= CAP, "coefficient capacity");
+  if (a.K != K) return cudaErrorInvalidValue;
+  const int zb = std::max(a.z_begin, K), ze = std::min(a.z_end, a.nz - K);
+  const int yrows = a.ny - 2 * K;
+  if (ze <= zb || yrows <= 0 || a.nx - 2 * K <= 0) return cudaSuccess;
+  Ssam3DParams<T, CAP> p;
+  std::memset(&p, 0, sizeof(p));
+  p.in = a.in;
+  p.out = a.out;
+  p.nx = a.nx;
+  p.ny = a.ny;
+  p.nz = a.nz;
+  const LanePlan lp = plan_lanes(M, Q);
+  p.e = lp.e;
+  p.G = lp.G;
+  p.A = lp.A;
+  p.V = lp.V;
+  p.nstrips = (a.nx + lp.V - 1) / lp.V;
+  p.ygroups = (yrows + RY - 1) / RY;
+  p.ring = K;
+  p.vec_ok = (a.nx % Q == 0) && aligned16(a.in) && aligned16(a.out);
+  const int zrows = ze - zb;
+  const long long per_z = static_cast<long long>(p.nstrips) * p.ygroups;
+  long long zsegs = (static_cast<long long>(kSMs) * 48 + per_z - 1) / per_z;
+  zsegs = std::max<long long>(1, std::min<long long>(zsegs, zrows));
+  int zseg = static_cast<int>((zrows + zsegs - 1) / zsegs);
+  zseg = std::max(zseg, std::min(zrows, 8 * (2 * K + 1)));
+  p.zseg = zseg;
+  p.z_begin = zb;
+  p.z_end = ze;
+  std::memcpy(p.coef, a.coef, sizeof(T) * M * M * M);
+  const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
+                  (zrows + zseg - 1) / zseg);
+  ssam3d_kernel<T, Q, K, Mask, RY, PFZ, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ssam_b200

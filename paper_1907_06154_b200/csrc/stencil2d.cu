@@ -1,0 +1,81 @@
+// stencil2d.cu -- one 2D Jacobi sweep on the SSAM engine.
+//
+// Reference: ssam::stencil2d, proj/include/ssam/kernels.hpp:231-277 with the
+// sparse window plans of :111-159 (taps bucketed by column, immediates as
+// coefficients, empty columns folded into the next shift).  Here the tap
+// footprint is a compile-time mask (StarMask2D for the star benchmarks
+// 2d5pt/2d9pt/.../2ds25pt, DenseMask otherwise) so empty cells cost nothing
+// and every coefficient is a constant-bank operand.  Orders above 6 use the
+// direct-gather kernel.
+#include "conv2d_impl.cuh"
+
+namespace ssam_b200 {
+
+template <class T>
+std::vector<T> dense2d_coef(const StencilDesc<T>& st) {
+  const int k = st.order, M = 2 * k + 1;
+  std::vector<T> c(static_cast<size_t>(M) * M, T(0));
+  for (size_t i = 0; i < st.taps.size(); ++i)
+    c[static_cast<size_t>(st.taps[i].dx + k) * M + (st.taps[i].dy + k)] = st.coeffs[i];
+  return c;
+}
+
+template <class T, int Q, int K, class Mask>
+cudaError_t st2d(const Engine2DArgs<T>& a, cudaStream_t s) {
+  constexpr int M = 2 * K + 1;
+  return launch_ssam2d<T, Q, M, M, Mask, pf_rows(M), M * M>(a, s);
+}
+
+template <class T, bool STAR>
+cudaError_t stencil2d_dispatch(const T* d_in, T* d_out, int W, int H, int y_begin, int y_end,
+                               const StencilDesc<T>& st, cudaStream_t s) {
+  constexpr int Q = Lanes<T>::Q;
+  const int k = st.order;
+  y_begin = std::max(y_begin, k);
+  y_end = std::min(y_end, H - k);
+  if (y_end <= y_begin || W - 2 * k <= 0) return cudaSuccess;
+  if (k > 6) return stencil2d_direct<T>(d_in, d_out, W, H, y_begin, y_end, st, s);
+  const std::vector<T> coef = dense2d_coef(st);
+  Engine2DArgs<T> a{d_in, d_out, W, H, 2 * k + 1, 2 * k + 1, coef.data(), kBndStencil, k,
+                    y_begin, y_end};
+  if constexpr (STAR) {
+    if (k >= 1 && classify2d(st.taps, k) == Shape2D::star) {
+      switch (k) {
+        case 1: return st2d<T, Q, 1, StarMask2D<1>>(a, s);
+        case 2: return st2d<T, Q, 2, StarMask2D<2>>(a, s);
+        case 3: return st2d<T, Q, 3, StarMask2D<3>>(a, s);
+        case 4: return st2d<T, Q, 4, StarMask2D<4>>(a, s);
+        case 5: return st2d<T, Q, 5, StarMask2D<5>>(a, s);
+        case 6: return st2d<T, Q, 6, StarMask2D<6>>(a, s);
+      }
+    }
+  }
+  switch (k) {
+    case 0: return st2d<T, Q, 0, DenseMask>(a, s);
+    case 1: return st2d<T, Q, 1, DenseMask>(a, s);
+    case 2: return st2d<T, Q, 2, DenseMask>(a, s);
+    case 3: return st2d<T, Q, 3, DenseMask>(a, s);
+    case 4: return st2d<T, Q, 4, DenseMask>(a, s);
+    case 5: return st2d<T, Q, 5, DenseMask>(a, s);
+    case 6: return st2d<T, Q, 6, DenseMask>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <>
+cudaError_t stencil2d_sweep<float>(const float* i, float* o, int W, int H, int yb, int ye,
+                                   const StencilDesc<float>& st, cudaStream_t s) {
+  return stencil2d_dispatch<float, true>(i, o, W, H, yb, ye, st, s);
+}
+template <>
+cudaError_t stencil2d_sweep<double>(const double* i, double* o, int W, int H, int yb, int ye,
+                                    const StencilDesc<double>& st, cudaStream_t s) {
+  return stencil2d_dispatch<double, true>(i, o, W, H, yb, ye, st, s);
+}
+template <>
+cudaError_t stencil2d_sweep<long long>(const long long* i, long long* o, int W, int H, int yb, int ye,
+                                       const StencilDesc<long long>& st, cudaStream_t s) {
+  return stencil2d_dispatch<long long, false>(i, o, W, H, yb, ye, st, s);
+}
+
+}  // namespace ssam_b200

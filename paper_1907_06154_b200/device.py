@@ -1,0 +1,120 @@
+"""Device-resident entry points (benchmarks, multi-GPU slabs).
+
+torch supplies device memory and streams (plumbing); every computation is a
+kernel in libssam_b200.so launched on the given (default: current) stream.
+Tensors must be contiguous CUDA tensors of float32, float64 or int64.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Tuple
+
+import numpy as np
+
+from . import (_DT, _StencilArgs, _lib, _raise, InvalidArgument, Stencil)
+
+_TORCH_DT = None
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _code(t) -> int:
+    torch = _torch()
+    m = {torch.float32: 0, torch.float64: 1, torch.int64: 2}
+    if t.dtype not in m:
+        raise InvalidArgument(f"unsupported dtype {t.dtype}")
+    if not t.is_cuda or not t.is_contiguous():
+        raise InvalidArgument("expected a contiguous CUDA tensor")
+    return m[t.dtype]
+
+
+def _np_dtype(code: int):
+    return {0: np.float32, 1: np.float64, 2: np.int64}[code]
+
+
+def _s(stream) -> int:
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def conv2d(d_in, d_out, weights, boundary: int = 0, y_begin: int = 0,
+           y_end: Optional[int] = None, stream=None) -> None:
+    """conv2d over output rows [y_begin, y_end) of (H, W) tensors."""
+    code = _code(d_in)
+    H, W = d_in.shape
+    w = np.ascontiguousarray(np.asarray(weights).astype(_np_dtype(code)))
+    _raise(_lib.ssam_b200_conv2d_device(code, d_in.data_ptr(), d_out.data_ptr(), W, H, y_begin,
+                                        H if y_end is None else y_end, w.ctypes.data,
+                                        w.shape[0], w.shape[1], int(boundary), _s(stream)))
+
+
+def stencil2d_sweep(d_in, d_out, st: Stencil, y_begin: int = 0, y_end: Optional[int] = None,
+                    stream=None) -> None:
+    code = _code(d_in)
+    H, W = d_in.shape
+    sa = _StencilArgs(st, _np_dtype(code))
+    _raise(_lib.ssam_b200_stencil2d_sweep(code, d_in.data_ptr(), d_out.data_ptr(), W, H, y_begin,
+                                          H if y_end is None else y_end, sa.ref, _s(stream)))
+
+
+def stencil2d_tb(d_in, d_out, st: Stencil, tb: int, stream=None) -> None:
+    code = _code(d_in)
+    H, W = d_in.shape
+    sa = _StencilArgs(st, _np_dtype(code))
+    _raise(_lib.ssam_b200_stencil2d_tb(code, d_in.data_ptr(), d_out.data_ptr(), W, H, sa.ref, tb,
+                                       _s(stream)))
+
+
+def stencil2d_tb_max(st: Stencil, dtype) -> int:
+    sa = _StencilArgs(st, dtype)
+    return int(_lib.ssam_b200_stencil2d_tb_max(_DT[np.dtype(dtype)], sa.ref))
+
+
+def stencil2d_run(d_a, d_b, st: Stencil, iters: int, tb: int = 0, stream=None):
+    """iters sweeps ping-ponging d_a/d_b; returns whichever holds the result."""
+    code = _code(d_a)
+    H, W = d_a.shape
+    sa = _StencilArgs(st, _np_dtype(code))
+    res = C.c_void_p()
+    _raise(_lib.ssam_b200_stencil2d_run(code, d_a.data_ptr(), d_b.data_ptr(), W, H, sa.ref,
+                                        iters, tb, _s(stream), C.byref(res)))
+    return d_a if res.value == d_a.data_ptr() else d_b
+
+
+def stencil3d_sweep(d_in, d_out, st: Stencil, z_begin: int = 0, z_end: Optional[int] = None,
+                    stream=None) -> None:
+    code = _code(d_in)
+    nz, ny, nx = d_in.shape
+    sa = _StencilArgs(st, _np_dtype(code))
+    _raise(_lib.ssam_b200_stencil3d_sweep(code, d_in.data_ptr(), d_out.data_ptr(), nx, ny, nz,
+                                          z_begin, nz if z_end is None else z_end, sa.ref,
+                                          _s(stream)))
+
+
+def stencil3d_run(d_a, d_b, st: Stencil, iters: int, stream=None):
+    code = _code(d_a)
+    nz, ny, nx = d_a.shape
+    sa = _StencilArgs(st, _np_dtype(code))
+    res = C.c_void_p()
+    _raise(_lib.ssam_b200_stencil3d_run(code, d_a.data_ptr(), d_b.data_ptr(), nx, ny, nz, sa.ref,
+                                        iters, _s(stream), C.byref(res)))
+    return d_a if res.value == d_a.data_ptr() else d_b
+
+
+def fill_random(t, seed: int, first: int = 0, stream=None) -> None:
+    """SplitMix64 fill bit-identical to random_grid2d/3d (element i = draw first+i)."""
+    _raise(_lib.ssam_b200_fill_random(_code(t), t.data_ptr(), t.numel(), seed, first,
+                                      _s(stream)))
+
+
+def max_rel_err(a, b, stream=None) -> Tuple[float, float]:
+    """(max |a-b|/max(1,|b|), max |a-b|) reduced on the device."""
+    rel, ab = C.c_double(), C.c_double()
+    _raise(_lib.ssam_b200_max_rel_err(_code(a), a.data_ptr(), b.data_ptr(), a.numel(),
+                                      C.byref(rel), C.byref(ab), _s(stream)))
+    return rel.value, ab.value

@@ -1,0 +1,70 @@
+"""C-ABI library: loads without a GPU, exports every declared symbol, and
+never computes on the CPU (CPU-only tests)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    with open(os.path.join(ROOT, "include", "ssam_b200.h")) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(ssam_b200_\w+)\s*\(", text)))
+
+
+def test_header_and_exports_agree(lib):
+    declared = declared_symbols()
+    assert declared, "no declarations parsed"
+    raw = ctypes.CDLL(lib.LIB_PATH)
+    for name in declared:
+        assert hasattr(raw, name), f"{name} declared in include/ssam_b200.h but not exported"
+    assert sorted(lib.EXPORTED) == declared
+
+
+def test_abi_version(lib):
+    assert lib.lib.ssam_b200_abi_version() == 1
+
+
+def test_default_config_matches_reference(lib):
+    c = lib._Cfg()
+    lib.lib.ssam_b200_default_config(ctypes.byref(c))
+    assert (c.p, c.b, c.boundary, c.lane_count, c.threads) == (4, 128, 0, 32, 0)
+
+
+def test_library_is_cuda_code(lib):
+    """The shared object carries sm_100a SASS for the SSAM kernels."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", lib.LIB_PATH], capture_output=True,
+                         text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+@pytest.mark.skipif(os.environ.get("CUDA_VISIBLE_DEVICES", None) == "" or False,
+                    reason="explicitly hidden devices")
+def test_no_cpu_fallback_without_device(lib):
+    if lib.device_available():
+        pytest.skip("a device is present; covered by the GPU tests")
+    g = np.zeros((64, 64), np.float32)
+    with pytest.raises(lib.NoDevice):
+        lib.conv2d(g, np.ones((3, 3), np.float32))
+    with pytest.raises(lib.NoDevice):
+        lib.stencil2d(g, lib.convert_stencil(lib.make_benchmark_stencil("2d5pt"), np.float32),
+                      lib.KernelConfig(), 1)
+
+
+def test_catalog_matches_golden(lib, golden):
+    assert lib.benchmark_stencil_names() == list(golden["catalog"].keys()) or \
+        sorted(lib.benchmark_stencil_names()) == sorted(golden["catalog"].keys())
+    for name, want in golden["catalog"].items():
+        st = lib.make_benchmark_stencil(name)
+        assert (st.dims, st.order, st.fpp) == (want["dims"], want["order"], want["fpp"])
+        assert [list(t.offset) for t in st.taps] == want["offsets"]
+        assert [float(t.coeff).hex() for t in st.taps] == want["coeffs"]
+    with pytest.raises(lib.InvalidArgument):
+        lib.make_benchmark_stencil("2d7pt")
