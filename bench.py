@@ -1,0 +1,502 @@
+#!/usr/bin/env python3
+"""bench.py -- SSAM engine benchmark (driver contract).
+
+Headline workload (BASELINE.json configs[4], the config its metric is quoted
+on "at 1/2/4/8 B200"): 3D 7-point Jacobi, fp32, on a 2048 x 2048 x (512*N)
+grid z-slab-sharded over N GPUs (one process per GPU, NCCL halo exchange of
+one 16 MiB plane per neighbour per sweep, overlapped with the interior).
+One step = `--iters` (default 100) sweeps of the whole grid.  Weak scaling:
+each GPU always owns 2048 x 2048 x 512 cells.
+
+  value   whole-job cell-updates per second (GCells/s), device-resident
+          inputs, CUDA events on the compute stream, max over ranks.
+  e2e     the same metric through the public C ABI with HOST buffers
+          (ssam_b200_stencil3d at N=1; the slab runner at N>1): pinned
+          host->device copy of the step's input, the sweeps, and the
+          device->host copy of the result inside the timed region.
+  roofline  the dominant kernel (ssam3d_kernel, 3d7pt fp32): algorithmic
+          bytes (4 B read + 4 B write per updated cell) / mean launch time.
+  kernels per-kernel GCells/s and %-of-peak for the other configs (conv
+          sweep 3x3..20x20, 2D stencils x100 sweeps, 3D stencils at 512^3),
+          rank 0 at N=1.
+  cpu_baseline  the reference's own CPU path (oracle/_ref, ssam::stencil3d,
+          all host threads) on a bounded sample of the same workload.
+
+--impl reference times that reference CPU path alone (rank 0; other ranks
+exit 0).  Data are synthetic: the reference's SplitMix64 stream generated on
+the device (bit-identical to random_grid3d), seed 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GCells/s and achieved HBM GB/s (% of peak) per kernel at 1/2/4/8 B200"
+NX = NY = 2048
+NZ_PER_GPU = 512
+STENCIL = "3d7pt"
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured", float(p.get("sm_max_mhz", 1965.0))
+    except Exception:
+        return 6650.0, "fallback", 1965.0
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (oracle/_ref) -- cpu_baseline and --impl reference
+# ---------------------------------------------------------------------------
+
+def reference_sample(seconds: float = 10.0, max_reps: int = 1000):
+    """ssam::stencil3d<float> 3d7pt (the reference's CPU SSAM path, all host
+    threads) on a 2048 x 2048 x 16 block of the same seeded grid, repeated
+    single sweeps until `seconds` of CPU work.  Returns (GCells/s, cores, sample)."""
+    import numpy as np
+    from oracle import Oracle, Reference
+    ref = Reference()
+    orc = Oracle()
+    st = ref.benchmark_stencil(STENCIL)
+    nz = 16
+    g = orc.random_grid((nz, NY, NX), np.float32, 0)
+    cf = st["coeffs"].astype(np.float32)
+    cells = 0
+    t0 = time.perf_counter()
+    reps = 0
+    while reps < max_reps:
+        rc, _, _ = ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128)
+        assert rc == 0
+        cells += g.size
+        reps += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return cells / dt / 1e9, ref.max_threads(), \
+        f"{reps} sweep(s) of 3d7pt f32 on a {NX}x{NY}x{nz} block (seed 0), ssam::stencil3d threads=0"
+
+
+def run_reference_arm(args, rank: int, world: int):
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import Oracle, Reference
+    ref = Reference()
+    orc = Oracle()
+    st = ref.benchmark_stencil(STENCIL)
+    nz = 16
+    g = orc.random_grid((nz, NY, NX), np.float32, 0)
+    cf = st["coeffs"].astype(np.float32)
+    for _ in range(args.warmup):
+        ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rc, _, _ = ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128)
+        assert rc == 0
+    dt = time.perf_counter() - t0
+    value = g.size * args.steps / dt / 1e9
+    sample = (f"each step: 1 sweep of 3d7pt f32 on a {NX}x{NY}x{nz} block of the workload "
+              f"(seed 0), ssam::stencil3d from oracle/_ref, threads=0")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GCells/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(world, args),
+        "cpu_baseline": {"value": round(value, 6), "unit": "GCells/s",
+                         "cores": ref.max_threads(), "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 6), "unit": "GCells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(world: int, args):
+    return {"workload": f"{STENCIL} f32 {NX}x{NY}x({NZ_PER_GPU}*N) z-slab, NVLink halo exchange",
+            "stencil": STENCIL, "nx": NX, "ny": NY, "nz": NZ_PER_GPU * world,
+            "nz_per_gpu": NZ_PER_GPU, "iters_per_step": args.iters, "temporal_block": 1,
+            "parallelism": f"z-slab x{world}", "seed": 0,
+            "l2": "no flush needed: 8 GiB per buffer >> 126 MB L2"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def run_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1907_06154_b200 as ssam
+    from paper_1907_06154_b200 import device as dev
+    from paper_1907_06154_b200.slab import SlabRunner, decompose, fill_slab
+
+    torch.cuda.set_device(local_rank)
+    peak, peak_kind, sm_max_nominal = load_peaks()
+    st = ssam.convert_stencil(ssam.make_benchmark_stencil(STENCIL), np.float32)
+    k = st.order
+    slab = decompose(NZ_PER_GPU * world, world, rank, k)
+    a = torch.empty((slab.nz_local, NY, NX), dtype=torch.float32, device="cuda")
+    fill_slab(a, slab, NX, NY, seed=0)
+    b = a.clone()
+    comm = torch.cuda.Stream() if world > 1 else None
+
+    launch_ms = []
+    timing = {"on": False}
+
+    def sweep(cur, nxt, zb, ze):
+        if ze <= zb:
+            return
+        if timing["on"] and zb == slab.compute_range()[0] and world == 1:
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            dev.stencil3d_sweep(cur, nxt, st, zb, ze)
+            e.record()
+            launch_ms.append((s, e))
+        else:
+            dev.stencil3d_sweep(cur, nxt, st, zb, ze)
+
+    runner = SlabRunner(slab, sweep, comm_stream=comm)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        runner.run(a, b, args.iters)
+    torch.cuda.synchronize()
+    barrier()
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    time.sleep(0.3)
+    n_launch0 = ssam.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    timing["on"] = True
+    t_start.record()
+    for _ in range(args.steps):
+        runner.run(a, b, args.iters)
+    t_end.record()
+    torch.cuda.synchronize()
+    timing["on"] = False
+    barrier()
+    clk = clocks.stop()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    launches = ssam.launch_count() - n_launch0
+
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    nl = torch.tensor([launches], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(nl, op=dist.ReduceOp.SUM)
+    max_ms = float(t.item())
+    total_cells = NX * NY * NZ_PER_GPU * world * args.iters * args.steps
+    value = total_cells / (max_ms / 1e3) / 1e9
+
+    # dominant kernel: ssam3d_kernel over the whole slab (N=1 timing by launch)
+    interior = (NX - 2 * k) * (NY - 2 * k)
+    lo, hi = slab.compute_range()
+    cells_per_launch = interior * (hi - lo)
+    if launch_ms:
+        durs = [s.elapsed_time(e) for s, e in launch_ms]
+        mean_ms = sum(durs) / len(durs)
+    else:
+        mean_ms = max_ms / (args.steps * args.iters)
+    achieved = 8.0 * cells_per_launch / (mean_ms / 1e3) / 1e9
+    traffic = load_traffic().get(f"ssam3d_{STENCIL}_f32_{NX}x{NY}x{slab.nz_local}")
+
+    # free the slab before the e2e / per-kernel phases
+    del a, b
+    torch.cuda.empty_cache()
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_slab(args, slab, st, world, rank)
+
+    kernels = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_suite:
+        kernels = kernel_suite(peak, sm_max_nominal)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            v, cores, sample = reference_sample(args.cpu_seconds)
+            cpu = {"value": round(v, 6), "unit": "GCells/s", "cores": cores, "kind": "reference",
+                   "sample": sample}
+        except Exception as ex:  # the reference build may be absent
+            cpu = {"value": None, "unit": "GCells/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GCells/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(max_ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference SplitMix64 stream, seed 0, generated on device)",
+            "config": workload_config(world, args),
+            "hbm_gbs_algorithmic": round(value * 8.0, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "peak_kind": peak_kind,
+                         "kernel": f"ssam3d_kernel {STENCIL} f32",
+                         "bytes_per_launch": 8 * cells_per_launch,
+                         "mean_launch_ms": round(mean_ms, 4)},
+            "e2e": e2e, "gpu_launches": int(nl.item()), "clocks": clk,
+            "cpu_baseline": cpu, "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def e2e_slab(args, slab, st, world, rank):
+    """Public-API end to end: pinned host input -> GPU -> host output per step."""
+    import numpy as np
+    import torch
+    import paper_1907_06154_b200 as ssam
+    from paper_1907_06154_b200.slab import SlabRunner
+    from paper_1907_06154_b200 import device as dev
+
+    nzl = slab.nz_local
+    host_in = torch.empty((nzl, NY, NX), dtype=torch.float32, pin_memory=True)
+    host_out = torch.empty((nzl, NY, NX), dtype=torch.float32, pin_memory=True)
+    tmp = torch.empty((nzl, NY, NX), dtype=torch.float32, device="cuda")
+    from paper_1907_06154_b200.slab import fill_slab
+    fill_slab(tmp, slab, NX, NY, seed=0)
+    host_in.copy_(tmp)
+    del tmp
+    torch.cuda.empty_cache()
+    steps = max(1, args.e2e_steps)
+    if world == 1:
+        import ctypes
+        cfg = ssam.KernelConfig(p=2, b=128)._c()
+        sa = ssam._StencilArgs(st, np.float32)
+
+        def one():
+            ssam._raise(ssam.lib.ssam_b200_stencil3d(
+                0, host_in.data_ptr(), NX, NY, nzl, sa.ref, ctypes.byref(cfg), args.iters,
+                host_out.data_ptr(), None))
+    else:
+        import torch.distributed as dist
+        comm = torch.cuda.Stream()
+        dev_a = torch.empty((nzl, NY, NX), dtype=torch.float32, device="cuda")
+        dev_b = torch.empty_like(dev_a)
+        runner = SlabRunner(slab, lambda c, n, zb, ze: dev.stencil3d_sweep(c, n, st, zb, ze),
+                            comm_stream=comm)
+
+        def one():
+            dev_a.copy_(host_in, non_blocking=True)
+            dev_b.copy_(dev_a)
+            res = runner.run(dev_a, dev_b, args.iters)
+            host_out.copy_(res, non_blocking=True)
+            torch.cuda.synchronize()
+
+    one()  # warm-up (pool allocation, first-touch of pinned pages)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    cells = NX * NY * NZ_PER_GPU * world * args.iters * steps
+    nbytes = nzl * NY * NX * 4
+    return {"value": round(cells / dt / 1e9, 3), "unit": "GCells/s",
+            "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
+            "steps": steps, "ms_per_step": round(dt / steps * 1e3, 3),
+            "api": "ssam_b200_stencil3d (C ABI, host buffers)" if world == 1 else
+                   "SlabRunner over ssam_b200_stencil3d_sweep (host buffers)"}
+
+
+def kernel_suite(peak, sm_mhz):
+    """Per-kernel throughput for the other BASELINE configs (device-resident)."""
+    import numpy as np
+    import torch
+    import paper_1907_06154_b200 as ssam
+    from paper_1907_06154_b200 import device as dev
+    from oracle import Oracle
+    orc = Oracle()
+    fp32_peak_tflops = 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+    def timed(fn, reps):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(reps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        return s.elapsed_time(e) / reps
+
+    out = {}
+    H = W = 8192
+    g = torch.empty((H, W), dtype=torch.float32, device="cuda")
+    dev.fill_random(g, 0)
+    o = torch.empty_like(g)
+    for K in range(3, 21):
+        f = orc.random_filter(K, K, np.float32, 1)
+        ms = timed(lambda: dev.conv2d(g, o, f), 5)
+        gc = H * W / ms / 1e6
+        out[f"conv2d_f32_8192_{K}x{K}"] = {
+            "gcells": round(gc, 2), "hbm_gbs": round(gc * 8, 1),
+            "hbm_frac": round(gc * 8 / peak, 4), "tflops": round(gc * 2 * K * K / 1e3, 2),
+            "fp32_frac": round(gc * 2 * K * K / 1e3 / fp32_peak_tflops, 4), "ms": round(ms, 4)}
+    del g, o
+    for dt, tdt, npdt, sz in (("f32", torch.float32, np.float32, 4),
+                              ("f64", torch.float64, np.float64, 8)):
+        a = torch.empty((H, W), dtype=tdt, device="cuda")
+        dev.fill_random(a, 0)
+        bb = torch.empty_like(a)
+        for name in ("2d5pt", "2d9pt", "2ds25pt"):
+            st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt)
+            iters = 100
+            ms = timed(lambda: dev.stencil2d_run(a, bb, st, iters), 1)
+            gc = H * W * iters / ms / 1e6
+            out[f"stencil2d_{name}_{dt}_8192_x100"] = {
+                "gcells": round(gc, 2), "hbm_gbs_equiv": round(gc * 2 * sz, 1),
+                "hbm_frac": round(gc * 2 * sz / peak, 4), "ms": round(ms, 3),
+                "tb": dev.stencil2d_tb_max(st, npdt)}
+        del a, bb
+    n = 512
+    for dt, tdt, npdt, sz in (("f32", torch.float32, np.float32, 4),
+                              ("f64", torch.float64, np.float64, 8)):
+        a = torch.empty((n, n, n), dtype=tdt, device="cuda")
+        dev.fill_random(a, 0)
+        bb = torch.empty_like(a)
+        for name in ("3d7pt", "3d13pt", "3d27pt", "poisson"):
+            st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt)
+            iters = 20
+            ms = timed(lambda: dev.stencil3d_run(a, bb, st, iters), 1)
+            gc = n ** 3 * iters / ms / 1e6
+            out[f"stencil3d_{name}_{dt}_512_x{iters}"] = {
+                "gcells": round(gc, 2), "hbm_gbs_equiv": round(gc * 2 * sz, 1),
+                "hbm_frac": round(gc * 2 * sz / peak, 4), "ms": round(ms, 3)}
+        del a, bb
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--iters", type=int, default=100, help="sweeps per step")
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-suite", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE",
+              file=sys.stderr)
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,163 @@
+"""Multi-GPU z-slab decomposition with halo exchange.
+
+One process per GPU.  A 3D grid of nz_global planes (x fastest,
+data[(z*ny + y)*nx + x], grid.hpp:30-49) is split along z -- the slowest
+axis, so every slab and every halo is a contiguous run of planes.  Rank r
+holds its owned planes plus `ghost` planes on each side:
+
+    local plane p  <->  global plane z_first - ghost + p,   p in [0, nz_own + 2*ghost)
+
+One sweep writes the owned planes that are interior to the GLOBAL domain
+(the global ring of width k is never written, exactly as
+oracle::stencil3d_naive leaves it), then the new boundary planes are swapped
+with the neighbours: my lowest `ghost` owned planes go to rank-1's top ghost
+slots, my highest to rank+1's bottom ghost slots.  That is the only exchange
+the path has -- a pairwise neighbour send/recv, not a reduction.
+
+Overlap (per sweep): the 2*ghost boundary planes are computed first, their
+exchange runs on a communication stream while the interior planes are
+computed, and the next sweep waits only for the receives.
+
+The exchange goes through torch.distributed (NCCL over NVLink on a B200 box,
+gloo on CPU for tests).  The sweep itself is pluggable so the CPU tests can
+drive the identical decomposition/exchange code with the oracle; in the
+product it is the CUDA z-streaming kernel (ssam_b200_stencil3d_sweep).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class Slab:
+    rank: int
+    world: int
+    nz_global: int
+    z_first: int   # first owned global plane
+    nz_own: int
+    ghost: int
+    order: int
+
+    @property
+    def nz_local(self) -> int:
+        return self.nz_own + 2 * self.ghost
+
+    def local(self, z_global: int) -> int:
+        return z_global - self.z_first + self.ghost
+
+    def compute_range(self):
+        """Local output planes of one sweep: owned ∩ global interior [k, nz-k)."""
+        lo = max(self.z_first, self.order)
+        hi = min(self.z_first + self.nz_own, self.nz_global - self.order)
+        return self.local(lo), self.local(max(lo, hi))
+
+    def boundary_ranges(self):
+        """(low, high) boundary plane ranges whose results neighbours need."""
+        lo, hi = self.compute_range()
+        g = self.ghost
+        low = (lo, min(hi, self.local(self.z_first) + g)) if self.rank > 0 else (lo, lo)
+        top_own = self.local(self.z_first + self.nz_own)
+        high = (max(lo, top_own - g), hi) if self.rank < self.world - 1 else (hi, hi)
+        return low, high
+
+
+def decompose(nz_global: int, world: int, rank: int, order: int, ghost: Optional[int] = None) -> Slab:
+    """Even split of nz_global planes over world ranks (the first
+    nz_global % world ranks own one extra plane)."""
+    g = order if ghost is None else ghost
+    base, extra = divmod(nz_global, world)
+    nz_own = base + (1 if rank < extra else 0)
+    z_first = rank * base + min(rank, extra)
+    if nz_own < g:
+        raise ValueError(f"slab of {nz_own} planes is thinner than the {g}-plane halo")
+    return Slab(rank, world, nz_global, z_first, nz_own, g, order)
+
+
+SweepFn = Callable[[torch.Tensor, torch.Tensor, int, int], None]  # (cur, nxt, z_begin, z_end)
+
+
+class SlabRunner:
+    """Runs Jacobi sweeps on one rank's slab with neighbour halo exchange."""
+
+    def __init__(self, slab: Slab, sweep: SweepFn, group=None, comm_stream=None):
+        self.slab = slab
+        self.sweep = sweep
+        self.group = group
+        self.cuda = comm_stream is not None
+        self.comm_stream = comm_stream
+
+    def _exchange(self, nxt: torch.Tensor) -> list:
+        s, g = self.slab, self.slab.ghost
+        if s.world == 1 or g == 0:
+            return []
+        ops = []
+        own_lo = s.local(s.z_first)
+        own_hi = own_lo + s.nz_own
+        if s.rank > 0:
+            ops.append(dist.P2POp(dist.isend, nxt[own_lo:own_lo + g], s.rank - 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, nxt[own_lo - g:own_lo], s.rank - 1, self.group))
+        if s.rank < s.world - 1:
+            ops.append(dist.P2POp(dist.isend, nxt[own_hi - g:own_hi], s.rank + 1, self.group))
+            ops.append(dist.P2POp(dist.irecv, nxt[own_hi:own_hi + g], s.rank + 1, self.group))
+        return dist.batch_isend_irecv(ops)
+
+    def step(self, cur: torch.Tensor, nxt: torch.Tensor) -> None:
+        """One sweep cur -> nxt including the halo exchange of nxt."""
+        s = self.slab
+        lo, hi = s.compute_range()
+        (bl0, bl1), (bh0, bh1) = s.boundary_ranges()
+        if s.world == 1:
+            self.sweep(cur, nxt, lo, hi)
+            return
+        # boundary planes first ...
+        if bl1 > bl0:
+            self.sweep(cur, nxt, bl0, bl1)
+        if bh1 > max(bh0, bl1):  # thin slabs: the two boundary bands may touch
+            self.sweep(cur, nxt, max(bh0, bl1), bh1)
+        if self.cuda:
+            main = torch.cuda.current_stream()
+            self.comm_stream.wait_stream(main)
+            with torch.cuda.stream(self.comm_stream):
+                reqs = self._exchange(nxt)
+            # ... interior while the halo is in flight
+            if bh0 > bl1:
+                self.sweep(cur, nxt, bl1, bh0)
+            for r in reqs:
+                r.wait()
+            main.wait_stream(self.comm_stream)
+        else:
+            reqs = self._exchange(nxt)
+            if bh0 > bl1:
+                self.sweep(cur, nxt, bl1, bh0)
+            for r in reqs:
+                r.wait()
+
+    def run(self, a: torch.Tensor, b: torch.Tensor, iters: int) -> torch.Tensor:
+        """iters sweeps; a holds the input, b must hold a copy of it (ring and
+        ghosts).  Returns the buffer with the final generation."""
+        cur, nxt = a, b
+        for _ in range(iters):
+            self.step(cur, nxt)
+            cur, nxt = nxt, cur
+        return cur
+
+
+def fill_slab(t: torch.Tensor, slab: Slab, nx: int, ny: int, seed: int) -> None:
+    """Fill a local slab buffer (owned + ghost planes) with the global
+    random_grid3d stream: local plane p is global plane z_first - ghost + p,
+    so every rank generates exactly its planes of the global grid."""
+    from .device import fill_random
+    plane = nx * ny
+    z0 = slab.z_first - slab.ghost
+    p0 = max(0, -z0)
+    p1 = min(slab.nz_local, slab.nz_global - z0)
+    if p1 > p0:
+        fill_random(t[p0:p1].view(-1), seed, first=(z0 + p0) * plane)
+    if p0 > 0:
+        t[:p0].zero_()
+    if p1 < slab.nz_local:
+        t[p1:].zero_()

@@ -1,0 +1,29 @@
+"""Launch one kernel config a few times (for ncu captures): prof_one.py KIND [args]
+   conv K | st2d NAME DT | st3d NAME DT N"""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_1907_06154_b200 as ssam
+from paper_1907_06154_b200 import device as dev
+kind = sys.argv[1]
+reps = 3
+if kind == "conv":
+    K = int(sys.argv[2]); H = W = 8192
+    g = torch.empty((H, W), dtype=torch.float32, device="cuda"); dev.fill_random(g, 0)
+    o = torch.empty_like(g)
+    f = np.random.default_rng(1).uniform(-1, 1, (K, K)).astype(np.float32)
+    for _ in range(reps): dev.conv2d(g, o, f)
+elif kind == "st2d":
+    name, dt = sys.argv[2], sys.argv[3]; H = W = 8192
+    tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)
+    a = torch.empty((H, W), dtype=tdt, device="cuda"); dev.fill_random(a, 0); b = a.clone()
+    st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt)
+    for _ in range(reps): dev.stencil2d_sweep(a, b, st)
+else:
+    name, dt, n = sys.argv[2], sys.argv[3], int(sys.argv[4])
+    tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)
+    nz = int(sys.argv[5]) if len(sys.argv) > 5 else n
+    a = torch.empty((nz, n, n), dtype=tdt, device="cuda"); dev.fill_random(a, 0); b = a.clone()
+    st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt)
+    for _ in range(reps): dev.stencil3d_sweep(a, b, st)
+torch.cuda.synchronize()
