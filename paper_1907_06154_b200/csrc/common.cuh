@@ -71,4 +71,72 @@ __device__ __forceinline__ void st_vec(T* p, const T (&in)[Q]) {
 
 __device__ __forceinline__ int clampi(int i, int n) { return i < 0 ? 0 : (i >= n ? n - 1 : i); }
 
+// ---------------------------------------------------------------------------
+// TMA bulk-copy staging (sm_90+/sm_100a): cp.async.bulk global -> shared,
+// completion tracked by a transaction-counting mbarrier per ring slot.  One
+// lane issues; the copy engine moves the bytes while the warp computes, so a
+// ring of D slots keeps D row loads in flight without holding registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+
+// Makes mbarrier initialisation visible to the async (TMA) proxy.
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Orders this thread's prior generic-proxy shared accesses (and those made
+// visible to it, e.g. by __syncwarp) before its subsequent async-proxy ops:
+// the WAR hand-off when a consumed slot is refilled by TMA.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 128-bit shared load of one lane's Q-vector.
+template <class T, int Q>
+__device__ __forceinline__ void lds_vec(const T* p, T (&out)[Q]) {
+  static_assert(sizeof(T) * Q == 16, "128-bit vectors only");
+  const int4 r = *reinterpret_cast<const int4*>(p);
+  VecT<T, Q> v;
+  memcpy(&v, &r, sizeof(r));
+#pragma unroll
+  for (int q = 0; q < Q; ++q) out[q] = v.v[q];
+}
+
 }  // namespace ssam_b200

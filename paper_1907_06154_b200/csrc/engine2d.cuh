@@ -162,13 +162,37 @@ __device__ __forceinline__ void store_row(const Ssam2DParams<T, CAP>& p, int y, 
     if (xres + q >= xlo && xres + q < xhi) row[xres + q] = acc[q];
 }
 
+template <class T, int Q, int NR, int MC, class Mask, int NB, int CAP>
+__device__ __forceinline__ void ssam_row(const T (&buf)[NB][Q], const Ssam2DParams<T, CAP>& p,
+                                         T (&acc)[Q]) {
+  if constexpr (MC > 0)
+    ssam_row_ct<T, Q, NR, MC, Mask, NB, CAP>(buf, p, acc);
+  else
+    ssam_row_rt<T, Q, NR, NB, CAP>(buf, p, acc);
+}
+
+// Dynamic shared memory of the TMA path: per warp D row slots + D mbarriers.
+template <class T, int Q, int D>
+__host__ __device__ constexpr size_t ring2d_bytes(int warps) {
+  return static_cast<size_t>(warps) * D * (32 * Q * sizeof(T) + 8);
+}
+
 // MC > 0: compile-time footprint with Mask; MC == 0: runtime p.M, dense.
-template <class T, int Q, int NR, int MC, class Mask, int PF, int CAP>
+//
+// Two load paths, chosen per launch (warp-uniform):
+//  * TMA ring (aligned grids, the benchmark path): lane 0 keeps D row copies
+//    in flight with cp.async.bulk into a per-warp shared ring; lanes read
+//    their 16-byte Q-vector with one LDS.128 and push it into the register
+//    window.  D rows of prefetch cost no registers.
+//  * direct loads (unaligned widths): 128-bit / scalar LDG with PF rows of
+//    register prefetch.
+template <class T, int Q, int NR, int MC, class Mask, int PF, int CAP, int D>
 __global__ void __launch_bounds__(128) ssam2d_kernel(const __grid_constant__ Ssam2DParams<T, CAP> p) {
-  constexpr int NB = NR + PF;
   constexpr int U = NR - 1 - (NR - 1) / 2;
+  constexpr int ROW = 32 * Q;
   const int lane = threadIdx.x & 31;
-  const int strip = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int wib = threadIdx.x >> 5;
+  const int strip = blockIdx.x * (blockDim.x >> 5) + wib;
   if (strip >= p.nstrips) return;
   const int y0 = p.y_begin + blockIdx.y * p.seg;
   const int y1 = min(y0 + p.seg, p.y_end);
@@ -176,8 +200,71 @@ __global__ void __launch_bounds__(128) ssam2d_kernel(const __grid_constant__ Ssa
   const int base = x_out0 - p.A;
   const int col0 = base + Q * lane;
   const int xres = col0 - p.G;
-  const bool fast = p.vec_ok && base >= 0 && base + 32 * Q <= p.W;
 
+  if (p.vec_ok) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(wib) * D * ROW;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(
+                         smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * ROW * sizeof(T)) +
+                     wib * D;
+    const bool interior_x = base >= 0 && base + ROW <= p.W;
+    const int cbeg = max(base, 0), cend = min(base + ROW, p.W);
+    const uint32_t bytes = static_cast<uint32_t>(cend - cbeg) * sizeof(T);
+    const int doff = cbeg - base;
+    if (lane == 0) {
+#pragma unroll
+      for (int s = 0; s < D; ++s) mbar_init(smem_u32(&bars[s]), 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+    const int count = (y1 - y0) + NR - 1;
+    auto issue = [&](int i) {
+      const int s = i % D;
+      const int r = clampi(y0 - U + i, p.H);
+      fence_proxy_async();
+      mbar_arrive_expect_tx(smem_u32(&bars[s]), bytes);
+      tma_load_1d(smem_u32(ring + s * ROW + doff), p.in + static_cast<size_t>(r) * p.W + cbeg,
+                  bytes, smem_u32(&bars[s]));
+    };
+    if (lane == 0)
+      for (int i = 0; i < min(D, count); ++i) issue(i);
+
+    T win[NR][Q];
+    for (int i = 0; i < count; ++i) {
+      const int s = i % D;
+      mbar_wait(smem_u32(&bars[s]), (i / D) & 1);
+#pragma unroll
+      for (int t = 0; t < NR - 1; ++t)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) win[t][q] = win[t + 1][q];
+      const T* slot = ring + s * ROW;
+      lds_vec<T, Q>(slot + Q * lane, win[NR - 1]);
+      const int r = y0 - U + i;
+      if (p.bmode == kBndZero && (r < 0 || r >= p.H)) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) win[NR - 1][q] = T(0);
+      } else if (p.bmode != kBndStencil && !interior_x) {
+        // conv edge strips: outside columns are zero or the clamped edge cell
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          const int x = col0 + q;
+          if (x < 0 || x >= p.W)
+            win[NR - 1][q] = p.bmode == kBndZero ? T(0) : slot[clampi(x, p.W) - base];
+        }
+      }
+      __syncwarp();
+      if (lane == 0 && i + D < count) issue(i + D);
+      if (i >= NR - 1) {
+        T acc[Q];
+        ssam_row<T, Q, NR, MC, Mask, NR, CAP>(win, p, acc);
+        store_row<T, Q, CAP>(p, y0 + i - (NR - 1), x_out0, xres, acc);
+      }
+    }
+    return;
+  }
+
+  constexpr int NB = NR + PF;
+  const bool fast = false;  // unaligned grids: scalar loads
   T buf[NB][Q];
 #pragma unroll
   for (int t = 0; t < NB - 1; ++t)
@@ -186,10 +273,7 @@ __global__ void __launch_bounds__(128) ssam2d_kernel(const __grid_constant__ Ssa
   for (int y = y0; y < y1; ++y) {
     load_row<T, Q>(p.in, p.W, p.H, y - U + NB - 1, col0, fast, p.bmode, buf[NB - 1]);
     T acc[Q];
-    if constexpr (MC > 0)
-      ssam_row_ct<T, Q, NR, MC, Mask, NB, CAP>(buf, p, acc);
-    else
-      ssam_row_rt<T, Q, NR, NB, CAP>(buf, p, acc);
+    ssam_row<T, Q, NR, MC, Mask, NB, CAP>(buf, p, acc);
     store_row<T, Q, CAP>(p, y, x_out0, xres, acc);
 #pragma unroll
     for (int t = 0; t < NB - 1; ++t)

@@ -12,6 +12,8 @@ namespace ssam_b200 {
 
 constexpr int kSMs = 148;          // B200: 2 dies x 74 SMs
 constexpr int kWarpsPerBlock = 4;  // 128-thread blocks
+constexpr int kRing2D = 8;         // TMA row slots in flight per warp (2D engine)
+constexpr int kRing3D = 4;         // TMA plane slots in flight per warp (3D engine)
 
 // Lane plan for an M-column footprint with Q columns per lane (engine2d.cuh):
 //   R = (M-1)/2, L = M-1-R; E extra shifts make the landing offset G a
@@ -81,7 +83,9 @@ cudaError_t launch_ssam2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   p.vec_ok = (a.W % Q == 0) && aligned16(a.in) && aligned16(a.out);
   std::memcpy(p.coef, a.coef, sizeof(T) * a.M * NR);
   const dim3 grid((p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock, (rows + p.seg - 1) / p.seg);
-  ssam2d_kernel<T, Q, NR, MC, Mask, PF, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
+  constexpr int D = kRing2D;
+  const size_t smem = p.vec_ok ? ring2d_bytes<T, Q, D>(kWarpsPerBlock) : 0;
+  ssam2d_kernel<T, Q, NR, MC, Mask, PF, CAP, D><<<grid, 32 * kWarpsPerBlock, smem, s>>>(p);
   note_launch();
   return cudaGetLastError();
 }
@@ -96,7 +100,7 @@ struct Engine3DArgs {
   int z_begin, z_end;
 };
 
-template <class T, int Q, int K, class Mask, int RY, int PFZ, int CAP>
+template <class T, int Q, int K, class Mask, int RY, int CAP>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
   static_assert(M * M * M <= CAP, "coefficient capacity");
@@ -132,7 +136,15 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   std::memcpy(p.coef, a.coef, sizeof(T) * M * M * M);
   const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
                   (zrows + zseg - 1) / zseg);
-  ssam3d_kernel<T, Q, K, Mask, RY, PFZ, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
+  constexpr int DZ = kRing3D;
+  const size_t smem = p.vec_ok ? ring3d_bytes<T, Q, RY, K, DZ>(kWarpsPerBlock) : 0;
+  auto kern = ssam3d_kernel<T, Q, K, Mask, RY, DZ, CAP>;
+  if (smem > 48 * 1024) {
+    const cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(p);
   note_launch();
   return cudaGetLastError();
 }

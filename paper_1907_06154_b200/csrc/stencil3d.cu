@@ -21,23 +21,22 @@ std::vector<T> dense3d_coef(const StencilDesc<T>& st) {
 }
 
 // Rows per warp and z-prefetch by (dtype, order): keeps the register cache
-// (2K+1+PFZ planes x (RY+2K) rows x Q columns) within ~100 registers.
+// (2K+1 planes x (RY+2K) rows x Q columns) within ~100 registers.
 template <class T, int K> struct Cfg3D;
-template <> struct Cfg3D<float, 0> { static constexpr int RY = 4, PFZ = 1; };
-template <> struct Cfg3D<float, 1> { static constexpr int RY = 4, PFZ = 0; };
-template <> struct Cfg3D<float, 2> { static constexpr int RY = 2, PFZ = 0; };
-template <> struct Cfg3D<double, 0> { static constexpr int RY = 4, PFZ = 1; };
-template <> struct Cfg3D<double, 1> { static constexpr int RY = 4, PFZ = 0; };
-template <> struct Cfg3D<double, 2> { static constexpr int RY = 2, PFZ = 0; };
-template <> struct Cfg3D<long long, 0> { static constexpr int RY = 4, PFZ = 1; };
-template <> struct Cfg3D<long long, 1> { static constexpr int RY = 4, PFZ = 0; };
-template <> struct Cfg3D<long long, 2> { static constexpr int RY = 2, PFZ = 0; };
+template <> struct Cfg3D<float, 0> { static constexpr int RY = 4; };
+template <> struct Cfg3D<float, 1> { static constexpr int RY = 4; };
+template <> struct Cfg3D<float, 2> { static constexpr int RY = 2; };
+template <> struct Cfg3D<double, 0> { static constexpr int RY = 4; };
+template <> struct Cfg3D<double, 1> { static constexpr int RY = 4; };
+template <> struct Cfg3D<double, 2> { static constexpr int RY = 2; };
+template <> struct Cfg3D<long long, 0> { static constexpr int RY = 4; };
+template <> struct Cfg3D<long long, 1> { static constexpr int RY = 4; };
+template <> struct Cfg3D<long long, 2> { static constexpr int RY = 2; };
 
-template <class T, int K, class Mask>
+template <class T, int K, class Mask, int RY = Cfg3D<T, K>::RY>
 cudaError_t st3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
-  return launch_ssam3d<T, Lanes<T>::Q, K, Mask, Cfg3D<T, K>::RY, Cfg3D<T, K>::PFZ, M * M * M>(a,
-                                                                                            s);
+  return launch_ssam3d<T, Lanes<T>::Q, K, Mask, RY, M * M * M>(a, s);
 }
 
 template <class T, bool SHAPES>
@@ -62,7 +61,7 @@ cudaError_t stencil3d_dispatch(const T* d_in, T* d_out, int nx, int ny, int nz, 
     case 1: return st3d<T, 1, DenseMask3>(a, s);
   }
   if constexpr (SHAPES) {
-    if (k == 2) return st3d<T, 2, DenseMask3>(a, s);
+    if (k == 2) return st3d<T, 2, DenseMask3, 1>(a, s);  // 125 taps: one row per warp
   }
   return cudaErrorInvalidValue;
 }
