@@ -43,11 +43,21 @@ __device__ __forceinline__ T shfl_up(T v, int d) { return __shfl_up_sync(kFull, 
 // element i takes element i-1.  Lane 0's first element keeps its own value
 // (shfl_up semantics, warp.hpp:59-77); it only ever feeds invalid outputs.
 template <class T, int Q>
-__device__ __forceinline__ void shift1(T (&a)[Q]) {
+__device__ __forceinline__ void shift_up1(T (&a)[Q]) {
   const T top = shfl_up(a[Q - 1], 1);
 #pragma unroll
   for (int q = Q - 1; q > 0; --q) a[q] = a[q - 1];
   a[0] = top;
+}
+
+// The mirror image: element i takes element i+1 (shfl_down; lane 31's last
+// element keeps its own value and only feeds invalid outputs).
+template <class T, int Q>
+__device__ __forceinline__ void shift_down1(T (&a)[Q]) {
+  const T bot = __shfl_down_sync(kFull, a[0], 1);
+#pragma unroll
+  for (int q = 0; q < Q - 1; ++q) a[q] = a[q + 1];
+  a[Q - 1] = bot;
 }
 
 // Read-only 128-bit load through the non-coherent path.
@@ -125,6 +135,63 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// 2D tiled TMA load of one box at element coordinates (x, y) of the tensor
+// map; out-of-bounds cells arrive as zeros.  The map lives in the kernel's
+// __grid_constant__ parameter block.
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int x, int y,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(tmap), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
+// Q-vector shared load / global store as 16-byte chunks (Q*sizeof(T) in {16, 32}).
+template <class T, int Q>
+__device__ __forceinline__ void lds_q(const T* p, T (&out)[Q]) {
+  constexpr int V = 16 / sizeof(T);
+  static_assert(Q % V == 0, "whole 16-byte chunks");
+#pragma unroll
+  for (int c = 0; c < Q / V; ++c) {
+    const int4 r = *reinterpret_cast<const int4*>(p + c * V);
+    T tmp[V];
+    memcpy(tmp, &r, 16);
+#pragma unroll
+    for (int q = 0; q < V; ++q) out[c * V + q] = tmp[q];
+  }
+}
+
+template <class T, int Q>
+__device__ __forceinline__ void st_q(T* p, const T (&in)[Q]) {
+  constexpr int V = 16 / sizeof(T);
+  static_assert(Q % V == 0, "whole 16-byte chunks");
+#pragma unroll
+  for (int c = 0; c < Q / V; ++c) {
+    int4 r;
+    memcpy(&r, in + c * V, 16);
+    *reinterpret_cast<int4*>(p + c * V) = r;
+  }
+}
+
+template <class T, int Q>
+__device__ __forceinline__ void ldg_q(const T* __restrict__ p, T (&out)[Q]) {
+  constexpr int V = 16 / sizeof(T);
+  static_assert(Q % V == 0, "whole 16-byte chunks");
+#pragma unroll
+  for (int c = 0; c < Q / V; ++c) {
+    const int4 r = __ldg(reinterpret_cast<const int4*>(p + c * V));
+    T tmp[V];
+    memcpy(tmp, &r, 16);
+#pragma unroll
+    for (int q = 0; q < V; ++q) out[c * V + q] = tmp[q];
   }
 }
 

@@ -23,6 +23,13 @@ std::vector<T> conv_coef(const T* w, int m, int n) {
   return c;
 }
 
+// Columns per lane: two 16-byte chunks for short fp32 filters (halves the
+// per-cell shuffle and loop overhead), one chunk otherwise.
+template <class T>
+constexpr int conv_q(int n) {
+  return sizeof(T) == 4 ? (n <= 7 ? 8 : 4) : 2;
+}
+
 template <class T, int Q, int N>
 cudaError_t conv_rt(const Engine2DArgs<T>& a, cudaStream_t s) {
   return launch_ssam2d<T, Q, N, 0, DenseMask, pf_rows(N), 20 * N>(a, s);
@@ -50,7 +57,7 @@ cudaError_t conv2d_dispatch(const T* d_in, T* d_out, int W, int H, int y_begin, 
     if (m == n) {
       switch (n) {
 #define X(K) \
-  case K: return conv_sq<T, Q, K>(a, s);
+  case K: return conv_sq<T, conv_q<T>(K), K>(a, s);
         SSAM_CONV_CASES(X)
 #undef X
       }
@@ -58,7 +65,7 @@ cudaError_t conv2d_dispatch(const T* d_in, T* d_out, int W, int H, int y_begin, 
   }
   switch (n) {
 #define X(N) \
-  case N: return conv_rt<T, Q, N>(a, s);
+  case N: return conv_rt<T, conv_q<T>(N), N>(a, s);
     SSAM_CONV_CASES(X)
 #undef X
   }

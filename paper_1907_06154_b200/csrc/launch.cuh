@@ -7,28 +7,27 @@
 #include "engine2d.cuh"
 #include "engine3d.cuh"
 #include "internal.hpp"
+#include "tmap.hpp"
 
 namespace ssam_b200 {
 
 constexpr int kSMs = 148;          // B200: 2 dies x 74 SMs
 constexpr int kWarpsPerBlock = 4;  // 128-thread blocks
-constexpr int kRing2D = 8;         // TMA row slots in flight per warp (2D engine)
-constexpr int kRing3D = 4;         // TMA plane slots in flight per warp (3D engine)
 
-// Lane plan for an M-column footprint with Q columns per lane (engine2d.cuh):
-//   R = (M-1)/2, L = M-1-R; E extra shifts make the landing offset G a
-//   multiple of Q; A (>= L, multiple of Q) is the left halo the warp loads;
-//   V = 32Q - G - A outputs per warp row, a multiple of Q.
+// Lane plan for an M-column footprint, Q columns per lane (engine2d.cuh).
+// R = (M-1)/2, L = M-1-R.  Lane 0 starts at the Q-aligned column
+// x_out0 - A; with the bidirectional chain every lane's result sits in its
+// own columns, valid where the L columns to the left and the R to the right
+// are inside the warp: [origin + L, origin + 32Q - R).  The warp owns the
+// Q-aligned run [x_out0, x_out0 + V) of that range.
 struct LanePlan {
-  int e, G, A, V;
+  int A, V;
 };
 inline LanePlan plan_lanes(int M, int Q) {
   const int R = (M - 1) / 2, L = M - 1 - R;
   LanePlan lp;
-  lp.e = (Q - R % Q) % Q;
-  lp.G = R + lp.e;
   lp.A = (L + Q - 1) / Q * Q;
-  lp.V = 32 * Q - lp.G - lp.A;
+  lp.V = (32 * Q - R - lp.A) / Q * Q;
   return lp;
 }
 
@@ -56,21 +55,30 @@ struct Engine2DArgs {
   int y_begin, y_end;
 };
 
+// TMA box depth: whole-window boxes (rotation by renaming) for short
+// windows, 4-row boxes otherwise; about a dozen rows in flight per warp.
+constexpr int box_rows(int nr) { return nr <= 8 ? nr : 4; }
+constexpr int box_ring(int nr, int q, int tsize) {
+  return std::max(2, ((q * tsize >= 32 ? 8 : 12) + box_rows(nr) - 1) / box_rows(nr));
+}
+
 template <class T, int Q, int NR, int MC, class Mask, int PF, int CAP>
 cudaError_t launch_ssam2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   static_assert(MC == 0 || MC * NR <= CAP, "coefficient capacity");
   if (a.M * NR > CAP || a.NR != NR || (MC > 0 && a.M != MC)) return cudaErrorInvalidValue;
   if (a.y_end <= a.y_begin) return cudaSuccess;
-  Ssam2DParams<T, CAP> p;
-  std::memset(&p, 0, sizeof(p));
+  constexpr int VQ = 16 / sizeof(T);
+  const bool tma = a.bmode != kBndReplicate && a.W % VQ == 0 && aligned16(a.in) &&
+                   aligned16(a.out);
+  Ssam2DTmaParams<T, CAP> P;
+  std::memset(&P, 0, sizeof(P));
+  Ssam2DParams<T, CAP>& p = P.p;
   p.in = a.in;
   p.out = a.out;
   p.W = a.W;
   p.H = a.H;
   p.M = a.M;
   const LanePlan lp = plan_lanes(a.M, Q);
-  p.e = lp.e;
-  p.G = lp.G;
   p.A = lp.A;
   p.V = lp.V;
   p.nstrips = (a.W + lp.V - 1) / lp.V;
@@ -83,9 +91,21 @@ cudaError_t launch_ssam2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   p.vec_ok = (a.W % Q == 0) && aligned16(a.in) && aligned16(a.out);
   std::memcpy(p.coef, a.coef, sizeof(T) * a.M * NR);
   const dim3 grid((p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock, (rows + p.seg - 1) / p.seg);
-  constexpr int D = kRing2D;
-  const size_t smem = p.vec_ok ? ring2d_bytes<T, Q, D>(kWarpsPerBlock) : 0;
-  ssam2d_kernel<T, Q, NR, MC, Mask, PF, CAP, D><<<grid, 32 * kWarpsPerBlock, smem, s>>>(p);
+  if (tma) {
+    constexpr int RB = box_rows(NR);
+    constexpr int D = box_ring(NR, Q, sizeof(T));
+    cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.W, a.H, sizeof(T) * a.W, 32 * Q, RB);
+    if (e != cudaSuccess) return e;
+    auto kern = ssam2d_tma_kernel<T, Q, NR, MC, Mask, RB, D, CAP>;
+    const size_t smem = tma2d_smem<T, Q, RB, D>(kWarpsPerBlock);
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(P);
+  } else {
+    ssam2d_kernel<T, Q, NR, MC, Mask, PF, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
+  }
   note_launch();
   return cudaGetLastError();
 }
@@ -100,6 +120,8 @@ struct Engine3DArgs {
   int z_begin, z_end;
 };
 
+constexpr int kRing3D = 3;  // TMA plane boxes in flight per warp (3D engine)
+
 template <class T, int Q, int K, class Mask, int RY, int CAP>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
@@ -108,16 +130,17 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   const int zb = std::max(a.z_begin, K), ze = std::min(a.z_end, a.nz - K);
   const int yrows = a.ny - 2 * K;
   if (ze <= zb || yrows <= 0 || a.nx - 2 * K <= 0) return cudaSuccess;
-  Ssam3DParams<T, CAP> p;
-  std::memset(&p, 0, sizeof(p));
+  constexpr int VQ = 16 / sizeof(T);
+  const bool tma = a.nx % VQ == 0 && aligned16(a.in) && aligned16(a.out);
+  Ssam3DTmaParams<T, CAP> P;
+  std::memset(&P, 0, sizeof(P));
+  Ssam3DParams<T, CAP>& p = P.p;
   p.in = a.in;
   p.out = a.out;
   p.nx = a.nx;
   p.ny = a.ny;
   p.nz = a.nz;
   const LanePlan lp = plan_lanes(M, Q);
-  p.e = lp.e;
-  p.G = lp.G;
   p.A = lp.A;
   p.V = lp.V;
   p.nstrips = (a.nx + lp.V - 1) / lp.V;
@@ -136,15 +159,23 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   std::memcpy(p.coef, a.coef, sizeof(T) * M * M * M);
   const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
                   (zrows + zseg - 1) / zseg);
-  constexpr int DZ = kRing3D;
-  const size_t smem = p.vec_ok ? ring3d_bytes<T, Q, RY, K, DZ>(kWarpsPerBlock) : 0;
-  auto kern = ssam3d_kernel<T, Q, K, Mask, RY, DZ, CAP>;
-  if (smem > 48 * 1024) {
-    const cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (tma) {
+    constexpr int NROW = RY + 2 * K;
+    constexpr int DZ = kRing3D;
+    cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
+                                 static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx, 32 * Q,
+                                 NROW);
     if (e != cudaSuccess) return e;
+    auto kern = ssam3d_tma_kernel<T, Q, K, Mask, RY, DZ, CAP>;
+    const size_t smem = ring3d_bytes<T, Q, RY, K, DZ>(kWarpsPerBlock);
+    if (smem > 48 * 1024) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(P);
+  } else {
+    ssam3d_kernel<T, Q, K, Mask, RY, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
   }
-  kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(p);
   note_launch();
   return cudaGetLastError();
 }

@@ -7,6 +7,8 @@
 // 2d5pt/2d9pt/.../2ds25pt, DenseMask otherwise) so empty cells cost nothing
 // and every coefficient is a constant-bank operand.  Orders above 6 use the
 // direct-gather kernel.
+#include <type_traits>
+
 #include "conv2d_impl.cuh"
 
 namespace ssam_b200 {
@@ -20,10 +22,18 @@ std::vector<T> dense2d_coef(const StencilDesc<T>& st) {
   return c;
 }
 
+// Columns per lane: 32 bytes for low orders, 16 bytes (one chunk) otherwise;
+// int64 (tests only) stays at one chunk.
+template <class T>
+constexpr int st_q(int k) {
+  return sizeof(T) == 4 ? (k <= 3 ? 8 : 4) : (std::is_same<T, double>::value && k <= 3 ? 4 : 2);
+}
+
 template <class T, int Q, int K, class Mask>
 cudaError_t st2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
-  return launch_ssam2d<T, Q, M, M, Mask, pf_rows(M), M * M>(a, s);
+  constexpr int QQ = st_q<T>(K);
+  return launch_ssam2d<T, QQ, M, M, Mask, pf_rows(M), M * M>(a, s);
 }
 
 template <class T, bool STAR>
