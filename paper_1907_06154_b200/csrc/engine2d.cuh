@@ -273,33 +273,66 @@ __global__ void __launch_bounds__(128)
   if (lane == 0)
     for (int j = 0; j < min(D, nbox); ++j) issue(j);
 
-  // RB == NR: stream row i sits in win[i % NR] and the window rotates by
-  // renaming; otherwise the window shifts down one row per step.
-  T win[NR][Q];
-  for (int j = 0; j < nbox; ++j) {
-    const int s = j % D;
-    mbar_wait(smem_u32(&bars[s]), (j / D) & 1);
-    const T* slot = ring + s * RB * ROW + Q * lane;
+  if constexpr (RB == NR) {
+    // Whole-window boxes: box j's NR rows are read into one half of a
+    // 2*NR-row register window in one burst of LDS (latency overlapped), then
+    // NR output rows are computed from the previous box's rows plus these.
+    // Two boxes per loop trip swap the halves' roles: no register moves.
+    T win[2 * NR][Q];
+    auto box = [&](int j, int cur) {
+      const int s = j % D;
+      mbar_wait(smem_u32(&bars[s]), (j / D) & 1);
+      const T* slot = ring + s * RB * ROW + Q * lane;
 #pragma unroll
-    for (int rr = 0; rr < RB; ++rr) {
-      const int i = j * RB + rr;
-      if (i >= count) break;
-      T acc[Q];
-      if constexpr (RB == NR) {
-        lds_q<T, Q>(slot + rr * ROW, win[rr]);
-        if (i >= NR - 1) ssam_row<T, Q, NR, MC, Mask, NR, CAP>(win, (rr + 1) % NR, p, acc);
-      } else {
+      for (int rr = 0; rr < NR; ++rr) lds_q<T, Q>(slot + rr * ROW, win[cur + rr]);
+      __syncwarp();  // every lane has read slot s before it is refilled
+      if (lane == 0 && j + D < nbox) issue(j + D);
+#pragma unroll
+      for (int rr = 0; rr < NR; ++rr) {
+        const int i = j * NR + rr;
+        if (i >= count) break;
+        if (i >= NR - 1) {
+          T acc[Q];
+          // window row t = stream row i-NR+1+t: rows of the previous box sit
+          // in the other half, so it is win[(cur + NR + rr + 1 + t) % 2NR]
+          ssam_row<T, Q, NR, MC, Mask, 2 * NR, CAP>(win, cur + NR + rr + 1, p, acc);
+          store_row<T, Q, CAP>(p, sp, y0 + i - (NR - 1), acc);
+        }
+      }
+    };
+    for (int j = 0; j < nbox; j += 2) {
+      box(j, 0);
+      if (j + 1 < nbox) box(j + 1, NR);
+    }
+  } else {
+    // Tall windows: 4-row boxes, the window shifts down one row per step.
+    T win[NR][Q];
+    for (int j = 0; j < nbox; ++j) {
+      const int s = j % D;
+      mbar_wait(smem_u32(&bars[s]), (j / D) & 1);
+      const T* slot = ring + s * RB * ROW + Q * lane;
+      T stg[RB][Q];
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr) lds_q<T, Q>(slot + rr * ROW, stg[rr]);
+      __syncwarp();
+      if (lane == 0 && j + D < nbox) issue(j + D);
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr) {
+        const int i = j * RB + rr;
+        if (i >= count) break;
 #pragma unroll
         for (int t = 0; t < NR - 1; ++t)
 #pragma unroll
           for (int q = 0; q < Q; ++q) win[t][q] = win[t + 1][q];
-        lds_q<T, Q>(slot + rr * ROW, win[NR - 1]);
-        if (i >= NR - 1) ssam_row<T, Q, NR, MC, Mask, NR, CAP>(win, 0, p, acc);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) win[NR - 1][q] = stg[rr][q];
+        if (i >= NR - 1) {
+          T acc[Q];
+          ssam_row<T, Q, NR, MC, Mask, NR, CAP>(win, 0, p, acc);
+          store_row<T, Q, CAP>(p, sp, y0 + i - (NR - 1), acc);
+        }
       }
-      if (i >= NR - 1) store_row<T, Q, CAP>(p, sp, y0 + i - (NR - 1), acc);
     }
-    __syncwarp();  // every lane has read slot s before it is refilled
-    if (lane == 0 && j + D < nbox) issue(j + D);
   }
 }
 

@@ -62,9 +62,11 @@ struct PoissonMask3 {
   }
 };
 
+// Shared memory of the TMA kernel: DZ plane boxes of (WPB*RY + 2K) rows
+// shared by the CTA's WPB warps, plus a full and an empty mbarrier per slot.
 template <class T, int Q, int RY, int K, int DZ>
 __host__ __device__ constexpr size_t ring3d_bytes(int warps) {
-  return static_cast<size_t>(warps) * DZ * ((RY + 2 * K) * 32 * Q * sizeof(T) + 8);
+  return static_cast<size_t>(DZ) * ((warps * RY + 2 * K) * 32 * Q * sizeof(T) + 16);
 }
 
 template <class T, int Q, int NROW>
@@ -171,9 +173,15 @@ __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], 
   }
 }
 
-// TMA kernel (16-byte aligned rows): one 2D tensor-map box of RY+2K rows per
-// input plane, DZ planes in flight per warp.  Out-of-range rows, planes and
-// columns arrive as zeros (interior outputs never read them).
+// TMA kernel (16-byte aligned rows).  The CTA's WPB warps cover WPB*RY
+// consecutive output rows of one x-strip and share one 2D tensor-map box of
+// WPB*RY + 2K rows per input plane (the y halo is fetched once per CTA, not
+// once per warp).  DZ plane slots form a ring guarded by a full barrier
+// (TMA transaction count) and an empty barrier (one arrival per warp).
+// Thread 0 produces: after consuming plane i it refills the slot of plane
+// i-1 -- one plane of slack so it rarely waits on the slowest warp.
+// Out-of-range rows, planes and columns arrive as zeros (interior outputs
+// never read them).
 template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP>
 __global__ void __launch_bounds__(128)
     ssam3d_tma_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
@@ -182,12 +190,13 @@ __global__ void __launch_bounds__(128)
   constexpr int NROW = RY + 2 * K;
   constexpr int NPL = M;
   constexpr int ROW = 32 * Q;
-  constexpr uint32_t BOX_BYTES = NROW * ROW * sizeof(T);
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int group = blockIdx.y * (blockDim.x >> 5) + wib;
-  if (group >= p.ygroups) return;
-  const int y_out0 = p.ring + group * RY;
+  const int wpb = blockDim.x >> 5;
+  const int brows = wpb * RY + 2 * K;
+  const uint32_t box_bytes = static_cast<uint32_t>(brows) * ROW * sizeof(T);
+  const int y_cta0 = p.ring + blockIdx.y * wpb * RY;
+  const int y_out0 = y_cta0 + wib * RY;
   const int z0 = p.z_begin + blockIdx.z * p.zseg;
   const int z1 = min(z0 + p.zseg, p.z_end);
   const int x_out0 = blockIdx.x * p.V;
@@ -197,37 +206,41 @@ __global__ void __launch_bounds__(128)
   const int count = (z1 - z0) + 2 * K;  // input planes z0-K .. z1-1+K
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  T* ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(wib) * DZ * NROW * ROW;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(
-                       smem_raw + static_cast<size_t>(blockDim.x >> 5) * DZ * BOX_BYTES) +
-                   wib * DZ;
-  if (lane == 0) {
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(DZ) * box_bytes);
+  uint64_t* empty = full + DZ;
+  if (threadIdx.x == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
-    for (int s = 0; s < DZ; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < DZ; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), wpb);
+    }
     fence_mbar_init();
   }
-  __syncwarp();
-  // Plane i of the stream (z = z0 - K + i): rows y_out0-K .. of the flattened
-  // (ny*nz)-row view; planes outside [0, nz) fall outside the view -> zeros.
+  __syncthreads();
+  // Plane i of the stream (z = z0 - K + i): rows y_cta0-K .. of the
+  // flattened (ny*nz)-row view; planes outside [0, nz) land outside -> zeros.
   auto issue = [&](int i) {
     const int s = i % DZ;
-    const uint32_t bar = smem_u32(&bars[s]);
+    if (i >= DZ) mbar_wait(smem_u32(&empty[s]), ((i / DZ) - 1) & 1);
+    const uint32_t bar = smem_u32(&full[s]);
     const int z = z0 - K + i;
-    const int row = (z >= 0 && z < p.nz) ? z * p.ny + (y_out0 - K) : -NROW;
-    mbar_arrive_expect_tx(bar, BOX_BYTES);
-    tma_load_2d(smem_u32(ring + s * NROW * ROW), &P.tmap, base, row, bar);
+    const int row = (z >= 0 && z < p.nz) ? z * p.ny + (y_cta0 - K) : -brows;
+    mbar_arrive_expect_tx(bar, box_bytes);
+    tma_load_2d(smem_u32(ring + static_cast<size_t>(s) * brows * ROW), &P.tmap, base, row, bar);
   };
-  if (lane == 0)
+  if (threadIdx.x == 0)
     for (int i = 0; i < min(DZ, count); ++i) issue(i);
   auto take = [&](int i, T (&dst)[NROW][Q]) {
     const int s = i % DZ;
-    mbar_wait(smem_u32(&bars[s]), (i / DZ) & 1);
-    const T* slot = ring + s * NROW * ROW + Q * lane;
+    mbar_wait(smem_u32(&full[s]), (i / DZ) & 1);
+    const T* slot = ring + (static_cast<size_t>(s) * brows + wib * RY) * ROW + Q * lane;
 #pragma unroll
     for (int r = 0; r < NROW; ++r) lds_q<T, Q>(slot + r * ROW, dst[r]);
     __syncwarp();
-    if (lane == 0 && i + DZ < count) issue(i + DZ);
+    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+    if (threadIdx.x == 0 && i >= 1 && i - 1 + DZ < count) issue(i - 1 + DZ);
   };
 
   T pl[NPL][NROW][Q];

@@ -59,7 +59,7 @@ struct Engine2DArgs {
 // windows, 4-row boxes otherwise; about a dozen rows in flight per warp.
 constexpr int box_rows(int nr) { return nr <= 8 ? nr : 4; }
 constexpr int box_ring(int nr, int q, int tsize) {
-  return std::max(2, ((q * tsize >= 32 ? 8 : 12) + box_rows(nr) - 1) / box_rows(nr));
+  return std::max(2, ((q * tsize >= 32 ? 6 : 10) + box_rows(nr) - 1) / box_rows(nr));
 }
 
 template <class T, int Q, int NR, int MC, class Mask, int PF, int CAP>
@@ -120,7 +120,7 @@ struct Engine3DArgs {
   int z_begin, z_end;
 };
 
-constexpr int kRing3D = 3;  // TMA plane boxes in flight per warp (3D engine)
+constexpr int kRing3D = 4;  // TMA plane slots per CTA ring (3D engine)
 
 template <class T, int Q, int K, class Mask, int RY, int CAP>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
@@ -160,11 +160,11 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
                   (zrows + zseg - 1) / zseg);
   if (tma) {
-    constexpr int NROW = RY + 2 * K;
+    constexpr int BROWS = kWarpsPerBlock * RY + 2 * K;  // one box per CTA per plane
     constexpr int DZ = kRing3D;
     cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
                                  static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx, 32 * Q,
-                                 NROW);
+                                 BROWS);
     if (e != cudaSuccess) return e;
     auto kern = ssam3d_tma_kernel<T, Q, K, Mask, RY, DZ, CAP>;
     const size_t smem = ring3d_bytes<T, Q, RY, K, DZ>(kWarpsPerBlock);
