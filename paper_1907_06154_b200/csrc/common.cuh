@@ -158,6 +158,32 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
+// Block until the shared-memory loads that produced rows[..] have returned
+// data.  A ring slot may only be handed back to the TMA unit once its reads
+// are PERFORMED -- issued is not enough: an LDS queued behind MIO traffic can
+// otherwise be overtaken by the refill (observed as whole corrupted boxes).
+// One register of every 16-byte chunk feeds an XOR chain whose result is
+// stored (volatile, to a per-lane scratch word): in-order issue then keeps
+// every later instruction -- the __syncwarp and the refill -- behind the
+// returned data.  Cheaper than fence.proxy.async (a MEMBAR) per box.
+template <class T, int Q, int N>
+__device__ __forceinline__ void wait_loaded(const T (&rows)[N][Q], int first, int count,
+                                            uint32_t scratch) {
+  constexpr int V = 16 / sizeof(T);
+  uint32_t dep = 0;
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    if (r < first || r >= first + count) continue;
+#pragma unroll
+    for (int c = 0; c < Q / V; ++c) {
+      uint32_t bits;
+      memcpy(&bits, &rows[r][c * V], sizeof(bits));
+      dep ^= bits;
+    }
+  }
+  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(scratch), "r"(dep) : "memory");
+}
+
 // Q-vector shared load / global store as 16-byte chunks (Q*sizeof(T) in {16, 32}).
 template <class T, int Q>
 __device__ __forceinline__ void lds_q(const T* p, T (&out)[Q]) {

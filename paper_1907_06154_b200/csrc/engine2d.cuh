@@ -227,10 +227,12 @@ __device__ __forceinline__ void store_row(const Ssam2DParams<T, CAP>& p, const S
     if (sp.x0 + q >= sp.xlo && sp.x0 + q < sp.xhi) row[q] = acc[q];
 }
 
-// Shared memory of the TMA kernel: per warp D boxes of RB rows + D mbarriers.
+// Shared memory of the TMA kernel: per warp D boxes of RB rows, D mbarriers
+// and a 32-word scratch line for wait_loaded().
 template <class T, int Q, int RB, int D>
 __host__ __device__ constexpr size_t tma2d_smem(int warps) {
-  return static_cast<size_t>(warps) * D * (static_cast<size_t>(RB) * 32 * Q * sizeof(T) + 8);
+  return static_cast<size_t>(warps) *
+         (D * (static_cast<size_t>(RB) * 32 * Q * sizeof(T) + 8) + 128);
 }
 
 template <class T, int Q, int NR, int MC, class Mask, int RB, int D, int CAP>
@@ -255,6 +257,9 @@ __global__ void __launch_bounds__(128)
   uint64_t* bars = reinterpret_cast<uint64_t*>(
                        smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * BOX_BYTES) +
                    wib * D;
+  const uint32_t scratch =
+      smem_u32(smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * (BOX_BYTES + 8)) +
+      (wib * 32 + lane) * 4;
   if (lane == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
@@ -285,6 +290,7 @@ __global__ void __launch_bounds__(128)
       const T* slot = ring + s * RB * ROW + Q * lane;
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) lds_q<T, Q>(slot + rr * ROW, win[cur + rr]);
+      wait_loaded<T, Q, 2 * NR>(win, cur, NR, scratch);
       __syncwarp();  // every lane has read slot s before it is refilled
       if (lane == 0 && j + D < nbox) issue(j + D);
 #pragma unroll
@@ -314,6 +320,7 @@ __global__ void __launch_bounds__(128)
       T stg[RB][Q];
 #pragma unroll
       for (int rr = 0; rr < RB; ++rr) lds_q<T, Q>(slot + rr * ROW, stg[rr]);
+      wait_loaded<T, Q, RB>(stg, 0, RB, scratch);
       __syncwarp();
       if (lane == 0 && j + D < nbox) issue(j + D);
 #pragma unroll

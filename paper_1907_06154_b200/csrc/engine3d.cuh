@@ -66,7 +66,8 @@ struct PoissonMask3 {
 // shared by the CTA's WPB warps, plus a full and an empty mbarrier per slot.
 template <class T, int Q, int RY, int K, int DZ>
 __host__ __device__ constexpr size_t ring3d_bytes(int warps) {
-  return static_cast<size_t>(DZ) * ((warps * RY + 2 * K) * 32 * Q * sizeof(T) + 16);
+  return static_cast<size_t>(DZ) * ((warps * RY + 2 * K) * 32 * Q * sizeof(T) + 16) +
+         static_cast<size_t>(warps) * 128;  // + wait_loaded() scratch
 }
 
 template <class T, int Q, int NROW>
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(128)
   T* ring = reinterpret_cast<T*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(DZ) * box_bytes);
   uint64_t* empty = full + DZ;
+  const uint32_t scratch = smem_u32(empty + DZ) + threadIdx.x * 4;
   if (threadIdx.x == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(128)
     const T* slot = ring + (static_cast<size_t>(s) * brows + wib * RY) * ROW + Q * lane;
 #pragma unroll
     for (int r = 0; r < NROW; ++r) lds_q<T, Q>(slot + r * ROW, dst[r]);
+    wait_loaded<T, Q, NROW>(dst, 0, NROW, scratch);
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
     if (threadIdx.x == 0 && i >= 1 && i - 1 + DZ < count) issue(i - 1 + DZ);
