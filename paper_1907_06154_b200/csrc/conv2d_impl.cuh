@@ -27,7 +27,7 @@ std::vector<T> conv_coef(const T* w, int m, int n) {
 // per-cell shuffle and loop overhead), one chunk otherwise.
 template <class T>
 constexpr int conv_q(int n) {
-  return sizeof(T) == 4 ? (n <= 7 ? 8 : 4) : 2;
+  return sizeof(T) == 4 ? (n <= 4 ? 8 : 4) : 2;
 }
 
 template <class T, int Q, int N>

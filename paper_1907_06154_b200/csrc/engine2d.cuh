@@ -311,34 +311,34 @@ __global__ void __launch_bounds__(128)
       if (j + 1 < nbox) box(j + 1, NR);
     }
   } else {
-    // Tall windows: 4-row boxes, the window shifts down one row per step.
+    // Tall windows: the window shifts down one row per step and exactly one
+    // row body is emitted (a large filter's row is thousands of FMAs; more
+    // unrolling only thrashes the instruction cache).  A slot is refilled
+    // after its last row was consumed by arithmetic, so its LDS are done.
     T win[NR][Q];
     for (int j = 0; j < nbox; ++j) {
       const int s = j % D;
       mbar_wait(smem_u32(&bars[s]), (j / D) & 1);
       const T* slot = ring + s * RB * ROW + Q * lane;
-      T stg[RB][Q];
-#pragma unroll
-      for (int rr = 0; rr < RB; ++rr) lds_q<T, Q>(slot + rr * ROW, stg[rr]);
-      wait_loaded<T, Q, RB>(stg, 0, RB, scratch);
-      __syncwarp();
-      if (lane == 0 && j + D < nbox) issue(j + D);
-#pragma unroll
-      for (int rr = 0; rr < RB; ++rr) {
+      const int rows = min(RB, count - j * RB);
+#pragma unroll 1
+      for (int rr = 0; rr < rows; ++rr) {
         const int i = j * RB + rr;
-        if (i >= count) break;
 #pragma unroll
         for (int t = 0; t < NR - 1; ++t)
 #pragma unroll
           for (int q = 0; q < Q; ++q) win[t][q] = win[t + 1][q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) win[NR - 1][q] = stg[rr][q];
+        lds_q<T, Q>(slot + rr * ROW, win[NR - 1]);
         if (i >= NR - 1) {
           T acc[Q];
           ssam_row<T, Q, NR, MC, Mask, NR, CAP>(win, 0, p, acc);
           store_row<T, Q, CAP>(p, sp, y0 + i - (NR - 1), acc);
+        } else {
+          wait_loaded<T, Q, NR>(win, NR - 1, 1, scratch);
         }
       }
+      __syncwarp();
+      if (lane == 0 && j + D < nbox) issue(j + D);
     }
   }
 }

@@ -184,7 +184,7 @@ __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], 
 // Out-of-range rows, planes and columns arrive as zeros (interior outputs
 // never read them).
 template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(256)
     ssam3d_tma_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
   const Ssam3DParams<T, CAP>& p = P.p;
   constexpr int M = 2 * K + 1;

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "engine2d.cuh"
@@ -55,11 +56,20 @@ struct Engine2DArgs {
   int y_begin, y_end;
 };
 
-// TMA box depth: whole-window boxes (rotation by renaming) for short
-// windows, 4-row boxes otherwise; about a dozen rows in flight per warp.
-constexpr int box_rows(int nr) { return nr <= 8 ? nr : 4; }
-constexpr int box_ring(int nr, int q, int tsize) {
-  return std::max(2, ((q * tsize >= 32 ? 6 : 10) + box_rows(nr) - 1) / box_rows(nr));
+// Taps of a compile-time footprint (MC == 0: runtime width, count as dense 20).
+template <class Mask>
+constexpr int mask_taps(int mc, int nr) {
+  int n = 0;
+  for (int j = 0; j < (mc > 0 ? mc : 20); ++j)
+    for (int t = 0; t < nr; ++t) n += Mask::has(j, t) ? 1 : 0;
+  return n;
+}
+// TMA box depth: whole-window boxes (ping-pong register windows, fully
+// unrolled) when the window is short and a row is light; otherwise 4-row
+// boxes with one row body per loop trip.  About 6-10 rows in flight per warp.
+constexpr int box_rows(int nr, int row_fmas) { return (nr <= 8 && row_fmas <= 256) ? nr : 4; }
+constexpr int box_ring(int rb, int q, int tsize) {
+  return std::max(2, ((q * tsize >= 32 ? 6 : 10) + rb - 1) / rb);
 }
 
 template <class T, int Q, int NR, int MC, class Mask, int PF, int CAP>
@@ -92,8 +102,8 @@ cudaError_t launch_ssam2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   std::memcpy(p.coef, a.coef, sizeof(T) * a.M * NR);
   const dim3 grid((p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock, (rows + p.seg - 1) / p.seg);
   if (tma) {
-    constexpr int RB = box_rows(NR);
-    constexpr int D = box_ring(NR, Q, sizeof(T));
+    constexpr int RB = box_rows(NR, mask_taps<Mask>(MC, NR) * Q);
+    constexpr int D = box_ring(RB, Q, sizeof(T));
     cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.W, a.H, sizeof(T) * a.W, 32 * Q, RB);
     if (e != cudaSuccess) return e;
     auto kern = ssam2d_tma_kernel<T, Q, NR, MC, Mask, RB, D, CAP>;
@@ -121,6 +131,16 @@ struct Engine3DArgs {
 };
 
 constexpr int kRing3D = 4;  // TMA plane slots per CTA ring (3D engine)
+
+// Warps per 3D CTA (each RY rows); SSAM_B200_3D_WPB overrides (4 or 8).
+inline int cta_warps_3d() {
+  static const int v = [] {
+    const char* e = std::getenv("SSAM_B200_3D_WPB");
+    const int w = e ? std::atoi(e) : 8;
+    return w >= 8 ? 8 : 4;
+  }();
+  return v;
+}
 
 template <class T, int Q, int K, class Mask, int RY, int CAP>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
@@ -157,23 +177,29 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   p.z_begin = zb;
   p.z_end = ze;
   std::memcpy(p.coef, a.coef, sizeof(T) * M * M * M);
-  const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
-                  (zrows + zseg - 1) / zseg);
   if (tma) {
-    constexpr int BROWS = kWarpsPerBlock * RY + 2 * K;  // one box per CTA per plane
+    // Taller CTAs share more of the y halo (2K rows per wpb*RY); the box
+    // must stay within TMA's 256-row limit and the ring within shared memory.
+    int wpb = cta_warps_3d();
+    while (wpb > 4 && (wpb * RY + 2 * K > 256 ||
+                       ring3d_bytes<T, Q, RY, K, kRing3D>(wpb) > 200 * 1024))
+      wpb /= 2;
+    const dim3 grid(p.nstrips, (p.ygroups + wpb - 1) / wpb, (zrows + zseg - 1) / zseg);
     constexpr int DZ = kRing3D;
     cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
                                  static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx, 32 * Q,
-                                 BROWS);
+                                 wpb * RY + 2 * K);
     if (e != cudaSuccess) return e;
     auto kern = ssam3d_tma_kernel<T, Q, K, Mask, RY, DZ, CAP>;
-    const size_t smem = ring3d_bytes<T, Q, RY, K, DZ>(kWarpsPerBlock);
+    const size_t smem = ring3d_bytes<T, Q, RY, K, DZ>(wpb);
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
-    kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(P);
+    kern<<<grid, 32 * wpb, smem, s>>>(P);
   } else {
+    const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
+                    (zrows + zseg - 1) / zseg);
     ssam3d_kernel<T, Q, K, Mask, RY, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
   }
   note_launch();

@@ -1,6 +1,7 @@
 // tmap.cpp -- TMA tensor maps for the SSAM streaming loaders.
 #include "tmap.hpp"
 
+#include <cstdlib>
 #include <mutex>
 
 namespace ssam_b200 {
@@ -24,6 +25,20 @@ EncodeFn encoder() {
   });
   return fn;
 }
+// L2 fetch granularity for box rows.  Box rows start 16-byte aligned inside
+// rows shared with neighbouring strips; SSAM_B200_L2PROMO (0/64/128/256)
+// overrides the default for experiments.
+CUtensorMapL2promotion l2_promotion() {
+  static const CUtensorMapL2promotion v = [] {
+    const char* e = std::getenv("SSAM_B200_L2PROMO");
+    const int b = e ? std::atoi(e) : 128;
+    return b >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+           : b >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+           : b >= 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                      : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  }();
+  return v;
+}
 }  // namespace
 
 cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uint64_t cols,
@@ -40,7 +55,7 @@ cudaError_t make_tmap_2d(CUtensorMap* map, const void* base, int elem_bytes, uin
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        l2_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
