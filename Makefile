@@ -18,7 +18,7 @@ CU_OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CPP_OBJS := $(BUILD)/abi.o $(BUILD)/tmap.o
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp) include/ssam_b200.h
 
-all: $(LIB) oracle
+all: $(LIB) oracle dropin
 
 $(BUILD)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -29,7 +29,7 @@ $(BUILD)/abi.o: $(SRC)/abi.cpp $(HDRS)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
-	$(NVCC) $(ARCH) -shared -cudart static $^ -o $@
+	$(NVCC) $(ARCH) -shared -cudart static -Xlinker -soname=libssam_b200.so $^ -o $@
 
 oracle:
 	$(MAKE) -C oracle
@@ -42,3 +42,20 @@ clean:
 $(BUILD)/tmap.o: $(SRC)/tmap.cpp $(HDRS)
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+# C++ drop-in parity test: the reference's own hot-path tests against
+# include/ssam_b200/kernels.hpp (types + oracle from the reference headers).
+REF ?= /root/reference/proj
+DROPIN := tests/cpp/bin/dropin_parity
+ifneq ($(wildcard $(REF)/include/ssam/oracle.hpp),)
+dropin: $(DROPIN)
+$(DROPIN): tests/cpp/dropin_parity.cpp include/ssam_b200/kernels.hpp include/ssam_b200.h $(LIB) oracle
+	@mkdir -p tests/cpp/bin
+	$(CXX) -std=c++20 -O2 -Iinclude -I$(REF)/include $< $(LIB) oracle/_ref/libssam_ref.so \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../../oracle/_ref' -o $@
+else
+dropin:
+	@echo "reference headers absent; keeping prebuilt $(DROPIN) (if any)"
+endif
+
+.PHONY: dropin
