@@ -246,3 +246,36 @@ def test_north_star_512_cubed(cuda_lib, orc, name, dt):
         got = res[z0:z1, y0:y1, x0:x1].cpu().numpy()
         worst = max(worst, max_rel_err(got, want))
     assert worst <= TOL[np.dtype(NP[dt])], worst
+
+
+# ---- temporal blocking (2D) ------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["2d5pt", "2d9pt"])
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_temporal_blocking_matches_sweeps(cuda_lib, orc, name, dt):
+    """TB fused sweeps == TB single sweeps (bit-for-bit: same per-cell
+    arithmetic) == the Jacobi oracle within tolerance, for every compiled
+    depth and iteration counts that leave remainders."""
+    import torch
+    from paper_1907_06154_b200 import device as dev
+    st = cuda_lib.convert_stencil(cuda_lib.make_benchmark_stencil(name), NP[dt])
+    tdt = torch.float32 if dt == "f32" else torch.float64
+    offs, cfs = taps_of(st)
+    cf = np.asarray(cfs, NP[dt])
+    tbmax = dev.stencil2d_tb_max(st, NP[dt])
+    assert tbmax >= 4
+    for (H, W) in ((260, 300), (97, 1024)):
+        g = orc.random_grid((H, W), NP[dt], 5)
+        for iters in (1, 3, 8, 13):
+            ref_a = torch.from_numpy(g).cuda()
+            ref_b = ref_a.clone()
+            single = dev.stencil2d_run(ref_a, ref_b, st, iters, tb=1).cpu().numpy()
+            want = orc.stencil2d(g, offs, cf, st.order, iters)
+            assert max_rel_err(single, want) <= TOL[np.dtype(NP[dt])]
+            for tb in (2, 4, 8):
+                if tb > tbmax:
+                    continue
+                a = torch.from_numpy(g).cuda()
+                b = a.clone()
+                got = dev.stencil2d_run(a, b, st, iters, tb=tb).cpu().numpy()
+                assert np.array_equal(got, single), (H, W, iters, tb)
