@@ -37,6 +37,66 @@ struct alignas(64) Tb2DParams {
   T coef[CAP];
 };
 
+// One stage's output row from its NR-row window (bidirectional chain, as in
+// engine2d.cuh); window row t <-> dy = t - K.
+// Window row t lives in register slot (rot + t) % NR (rotation by index,
+// `rot` folds to a constant after unrolling).
+template <class T, int Q, int K, class Mask, int CAP>
+__device__ __forceinline__ void tb_stage_row(const T (&w)[2 * K + 1][Q], int rot,
+                                             const Tb2DParams<T, CAP>& p, T (&acc)[Q]) {
+  constexpr int NR = 2 * K + 1;
+  auto colpart = [&](int j, T (&cp)[Q]) -> bool {
+    bool any = false;
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      if (Mask::has(j, t)) {
+        const T c = p.coef[j * NR + t];
+        const int b = (rot + t) % NR;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) cp[q] = any ? fma_t(c, w[b][q], cp[q]) : c * w[b][q];
+        any = true;
+      }
+    }
+    return any;
+  };
+#pragma unroll
+  for (int j = 0; j <= K; ++j) {
+    T cp[Q];
+    const bool any = colpart(j, cp);
+    if (j == 0) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
+    } else {
+      shift_up1<T, Q>(acc);
+      if (any) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[q] += cp[q];
+      }
+    }
+  }
+  if constexpr (K > 0) {
+    T accr[Q];
+#pragma unroll
+    for (int j = NR - 1; j > K; --j) {
+      T cp[Q];
+      const bool any = colpart(j, cp);
+      if (j == NR - 1) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
+      } else {
+        shift_down1<T, Q>(accr);
+        if (any) {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) accr[q] += cp[q];
+        }
+      }
+    }
+    shift_down1<T, Q>(accr);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] += accr[q];
+  }
+}
+
 template <class T, int Q, int K, class Mask, int TB, int RB, int D, int CAP>
 __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DParams<T, CAP> p) {
   constexpr int NR = 2 * K + 1;
@@ -81,83 +141,35 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
 
   // Per stage: the NR rows of its input generation; window row t <-> dy = t-K.
   T win[TB][NR][Q];
-  // Column partial of filter column j for stage s.
-  auto colpart = [&](int s, int j, T (&cp)[Q]) -> bool {
-    bool any = false;
-#pragma unroll
-    for (int t = 0; t < NR; ++t) {
-      if (Mask::has(j, t)) {
-        const T c = p.coef[j * NR + t];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) cp[q] = any ? fma_t(c, win[s][t][q], cp[q]) : c * win[s][t][q];
-        any = true;
-      }
-    }
-    return any;
-  };
   for (int j = 0; j < nbox; ++j) {
     const int s = j % D;
     mbar_wait(smem_u32(&bars[s]), (j / D) & 1);
     const T* slot = ring + s * RB * ROW + Q * lane;
-    const int rows = min(RB, count - j * RB);
-#pragma unroll 1
-    for (int rr = 0; rr < rows; ++rr) {
-      const int r = yin0 + j * RB + rr;  // input row entering stage 1
+    // RB == NR: stream row i lands in register slot i % NR = rr of every
+    // stage's window, and window row t is slot (rr + 1 + t) % NR -- the
+    // windows rotate by renaming, one fully unrolled box per loop trip.
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      const int i = j * RB + rr;
+      if (i >= count) break;
+      const int r = yin0 + i;  // input row entering stage 1
       T in_row[Q];
       lds_q<T, Q>(slot + rr * ROW, in_row);
 #pragma unroll
       for (int st = 0; st < TB; ++st) {
         // push the stage input row, then compute gen-(st+1) row r - (st+1)K
 #pragma unroll
-        for (int t = 0; t < NR - 1; ++t)
-#pragma unroll
-          for (int q = 0; q < Q; ++q) win[st][t][q] = win[st][t + 1][q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) win[st][NR - 1][q] = in_row[q];
+        for (int q = 0; q < Q; ++q) win[st][rr][q] = in_row[q];
         const int y = r - (st + 1) * K;
         T acc[Q];
-#pragma unroll
-        for (int jj = 0; jj <= K; ++jj) {
-          T cp[Q];
-          const bool any = colpart(st, jj, cp);
-          if (jj == 0) {
-#pragma unroll
-            for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
-          } else {
-            shift_up1<T, Q>(acc);
-            if (any) {
-#pragma unroll
-              for (int q = 0; q < Q; ++q) acc[q] += cp[q];
-            }
-          }
-        }
-        if constexpr (K > 0) {
-          T accr[Q];
-#pragma unroll
-          for (int jj = NR - 1; jj > K; --jj) {
-            T cp[Q];
-            const bool any = colpart(st, jj, cp);
-            if (jj == NR - 1) {
-#pragma unroll
-              for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
-            } else {
-              shift_down1<T, Q>(accr);
-              if (any) {
-#pragma unroll
-                for (int q = 0; q < Q; ++q) accr[q] += cp[q];
-              }
-            }
-          }
-          shift_down1<T, Q>(accr);
-#pragma unroll
-          for (int q = 0; q < Q; ++q) acc[q] += accr[q];
-        }
+        tb_stage_row<T, Q, K, Mask, CAP>(win[st], rr + 1, p, acc);
         // ring cells keep their (generation-invariant) value
         const bool row_ring = y < p.ring || y >= p.H - p.ring;
+        const int c = (rr + 1 + K) % NR;  // centre row slot
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
           const int x = x0 + q;
-          if (row_ring || x < xlo || x >= xhi) acc[q] = win[st][K][q];
+          if (row_ring || x < xlo || x >= xhi) acc[q] = win[st][c][q];
           in_row[q] = acc[q];
         }
       }
@@ -194,8 +206,8 @@ template <class T, int Q, int K, class Mask, int TB>
 cudaError_t launch_tb(const T* in, T* out, int W, int H, const StencilDesc<T>& st,
                       cudaStream_t s) {
   constexpr int NR = 2 * K + 1;
-  constexpr int RB = 4;
-  constexpr int D = 3;
+  constexpr int RB = NR;                 // whole-window boxes (rotation by renaming)
+  constexpr int D = (12 + RB - 1) / RB;  // ~12 rows in flight per warp
   constexpr int CAP = NR * NR;
   Tb2DParams<T, CAP> p;
   std::memset(&p, 0, sizeof(p));
@@ -272,7 +284,7 @@ template cudaError_t stencil2d_tb<long long>(const long long*, long long*, int, 
 // Deepest fused depth for automatic scheduling (1 = none).
 int stencil2d_tb_max(int dtype, int order, bool star) {
   if (dtype == 2 || !star) return 1;
-  if (order == 1) return 8;
+  if (order == 1) return 4;  // TB=8 is compiled but measured slower (register pressure)
   if (order == 2) return 4;
   return 1;
 }
