@@ -253,9 +253,10 @@ def test_north_star_512_cubed(cuda_lib, orc, name, dt):
 @pytest.mark.parametrize("name", ["2d5pt", "2d9pt"])
 @pytest.mark.parametrize("dt", ["f32", "f64"])
 def test_temporal_blocking_matches_sweeps(cuda_lib, orc, name, dt):
-    """TB fused sweeps == TB single sweeps (bit-for-bit: same per-cell
-    arithmetic) == the Jacobi oracle within tolerance, for every compiled
-    depth and iteration counts that leave remainders."""
+    """TB fused sweeps agree with TB single sweeps and with the Jacobi oracle
+    within tolerance, for every compiled depth and iteration counts that
+    leave remainders.  (Not bit-for-bit: the compiler may contract a
+    single-tap column's mul+add into one FMA in one kernel and not the other.)"""
     import torch
     from paper_1907_06154_b200 import device as dev
     st = cuda_lib.convert_stencil(cuda_lib.make_benchmark_stencil(name), NP[dt])
@@ -278,4 +279,9 @@ def test_temporal_blocking_matches_sweeps(cuda_lib, orc, name, dt):
                 a = torch.from_numpy(g).cuda()
                 b = a.clone()
                 got = dev.stencil2d_run(a, b, st, iters, tb=tb).cpu().numpy()
-                assert np.array_equal(got, single), (H, W, iters, tb)
+                assert max_rel_err(got, want) <= TOL[np.dtype(NP[dt])], (H, W, iters, tb)
+                assert max_rel_err(got, single) <= 4 * np.finfo(NP[dt]).eps * iters, \
+                    (H, W, iters, tb)
+                ring = np.ones_like(g, dtype=bool)
+                ring[st.order:-st.order, st.order:-st.order] = False
+                assert np.array_equal(got[ring], g[ring])
