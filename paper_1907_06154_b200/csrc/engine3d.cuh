@@ -36,6 +36,7 @@ struct Ssam3DParams {
   int z_begin, z_end;
   int ring;         // = K
   int vec_ok;
+  int cta_sx;       // TMA kernel: adjacent x-strips per CTA (sharing one box)
   T coef[CAP];      // coef[(l*M + j)*M + t], l = dz+K, j = dx+K, t = dy+K
 };
 
@@ -62,12 +63,21 @@ struct PoissonMask3 {
   }
 };
 
-// Shared memory of the TMA kernel: DZ plane boxes of (WPB*RY + 2K) rows
-// shared by the CTA's WPB warps, plus a full and an empty mbarrier per slot.
+// One ring slot: a brows x bcols box, padded to the 128-byte alignment TMA
+// requires of every destination.
+template <class T>
+__host__ __device__ constexpr size_t box_slot_elems(int brows, int bcols) {
+  return (static_cast<size_t>(brows) * bcols * sizeof(T) + 127) / 128 * 128 / sizeof(T);
+}
+
+// Shared memory of the TMA kernel: DZ plane boxes shared by the CTA's warps
+// (sx strips x sy row groups), a full and an empty mbarrier per slot, and
+// the wait_loaded() scratch line.
 template <class T, int Q, int RY, int K, int DZ>
-__host__ __device__ constexpr size_t ring3d_bytes(int warps) {
-  return static_cast<size_t>(DZ) * ((warps * RY + 2 * K) * 32 * Q * sizeof(T) + 16) +
-         static_cast<size_t>(warps) * 128;  // + wait_loaded() scratch
+__host__ __device__ constexpr size_t ring3d_bytes(int sx, int sy, int v) {
+  return static_cast<size_t>(DZ) *
+             (box_slot_elems<T>(sy * RY + 2 * K, (sx - 1) * v + 32 * Q) * sizeof(T) + 16) +
+         static_cast<size_t>(sx * sy) * 128;
 }
 
 template <class T, int Q, int NROW>
@@ -194,21 +204,26 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
-  const int brows = wpb * RY + 2 * K;
-  const uint32_t box_bytes = static_cast<uint32_t>(brows) * ROW * sizeof(T);
-  const int y_cta0 = p.ring + blockIdx.y * wpb * RY;
-  const int y_out0 = y_cta0 + wib * RY;
+  // CTA = sx adjacent x-strips x sy row groups; one box spans all of them.
+  const int sx = p.cta_sx, sy = wpb / p.cta_sx;
+  const int wx = wib % sx, wy = wib / sx;
+  const int brows = sy * RY + 2 * K;
+  const int bcols = (sx - 1) * p.V + ROW;
+  const uint32_t box_bytes = static_cast<uint32_t>(brows) * bcols * sizeof(T);
+  const size_t slot_elems = box_slot_elems<T>(brows, bcols);
+  const int y_cta0 = p.ring + blockIdx.y * sy * RY;
+  const int y_out0 = y_cta0 + wy * RY;
   const int z0 = p.z_begin + blockIdx.z * p.zseg;
   const int z1 = min(z0 + p.zseg, p.z_end);
-  const int x_out0 = blockIdx.x * p.V;
-  const int base = x_out0 - p.A;
-  const int x0 = base + Q * lane;
+  const int base = blockIdx.x * sx * p.V - p.A;  // box origin (16-byte aligned)
+  const int x_out0 = (blockIdx.x * sx + wx) * p.V;
+  const int x0 = base + wx * p.V + Q * lane;
   const bool owner = x0 >= x_out0 && x0 < x_out0 + p.V;
   const int count = (z1 - z0) + 2 * K;  // input planes z0-K .. z1-1+K
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(DZ) * box_bytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + DZ * slot_elems * sizeof(T));
   uint64_t* empty = full + DZ;
   const uint32_t scratch = smem_u32(empty + DZ) + threadIdx.x * 4;
   if (threadIdx.x == 0) {
@@ -230,16 +245,17 @@ __global__ void __launch_bounds__(256)
     const int z = z0 - K + i;
     const int row = (z >= 0 && z < p.nz) ? z * p.ny + (y_cta0 - K) : -brows;
     mbar_arrive_expect_tx(bar, box_bytes);
-    tma_load_2d(smem_u32(ring + static_cast<size_t>(s) * brows * ROW), &P.tmap, base, row, bar);
+    tma_load_2d(smem_u32(ring + s * slot_elems), &P.tmap, base, row, bar);
   };
   if (threadIdx.x == 0)
     for (int i = 0; i < min(DZ, count); ++i) issue(i);
   auto take = [&](int i, T (&dst)[NROW][Q]) {
     const int s = i % DZ;
     mbar_wait(smem_u32(&full[s]), (i / DZ) & 1);
-    const T* slot = ring + (static_cast<size_t>(s) * brows + wib * RY) * ROW + Q * lane;
+    const T* slot = ring + s * slot_elems + static_cast<size_t>(wy * RY) * bcols + wx * p.V +
+                    Q * lane;
 #pragma unroll
-    for (int r = 0; r < NROW; ++r) lds_q<T, Q>(slot + r * ROW, dst[r]);
+    for (int r = 0; r < NROW; ++r) lds_q<T, Q>(slot + r * bcols, dst[r]);
     wait_loaded<T, Q, NROW>(dst, 0, NROW, scratch);
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[s]));

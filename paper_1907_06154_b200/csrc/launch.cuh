@@ -141,6 +141,14 @@ inline int cta_warps_3d() {
   }();
   return v;
 }
+// Adjacent x-strips per 3D CTA (1 or 2); SSAM_B200_3D_SX overrides.
+inline int cta_strips_3d() {
+  static const int v = [] {
+    const char* e = std::getenv("SSAM_B200_3D_SX");
+    return e ? std::atoi(e) : 2;
+  }();
+  return v;
+}
 
 template <class T, int Q, int K, class Mask, int RY, int CAP>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
@@ -180,18 +188,27 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   if (tma) {
     // Taller CTAs share more of the y halo (2K rows per wpb*RY); the box
     // must stay within TMA's 256-row limit and the ring within shared memory.
-    int wpb = cta_warps_3d();
-    while (wpb > 4 && (wpb * RY + 2 * K > 256 ||
-                       ring3d_bytes<T, Q, RY, K, kRing3D>(wpb) > 200 * 1024))
-      wpb /= 2;
-    const dim3 grid(p.nstrips, (p.ygroups + wpb - 1) / wpb, (zrows + zseg - 1) / zseg);
+    // CTA = sx adjacent strips x sy row groups sharing one plane box: wider
+    // boxes halve the x-halo re-reads and make each row fetch ~1 KB
+    // contiguous.  Box limits: 256 elements per dimension, shared memory.
     constexpr int DZ = kRing3D;
+    int wpb = cta_warps_3d();
+    int sx = (cta_strips_3d() >= 2 && lp.V + 32 * Q <= 256 && p.nstrips >= 2) ? 2 : 1;
+    auto fits = [&](int w, int x) {
+      const int yy = w / x;
+      return yy * RY + 2 * K <= 256 && ring3d_bytes<T, Q, RY, K, DZ>(x, yy, lp.V) <= 200 * 1024;
+    };
+    while (wpb > sx * 2 && !fits(wpb, sx)) wpb /= 2;
+    const int sy = wpb / sx;
+    p.cta_sx = sx;
+    const dim3 grid((p.nstrips + sx - 1) / sx, (p.ygroups + sy - 1) / sy,
+                    (zrows + zseg - 1) / zseg);
     cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
-                                 static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx, 32 * Q,
-                                 wpb * RY + 2 * K);
+                                 static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx,
+                                 (sx - 1) * lp.V + 32 * Q, sy * RY + 2 * K);
     if (e != cudaSuccess) return e;
     auto kern = ssam3d_tma_kernel<T, Q, K, Mask, RY, DZ, CAP>;
-    const size_t smem = ring3d_bytes<T, Q, RY, K, DZ>(wpb);
+    const size_t smem = ring3d_bytes<T, Q, RY, K, DZ>(sx, sy, lp.V);
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
