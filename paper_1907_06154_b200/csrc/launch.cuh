@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "engine2d.cuh"
 #include "engine3d.cuh"
@@ -136,8 +137,8 @@ constexpr int kRing3D = 4;  // TMA plane slots per CTA ring (3D engine)
 inline int cta_warps_3d() {
   static const int v = [] {
     const char* e = std::getenv("SSAM_B200_3D_WPB");
-    const int w = e ? std::atoi(e) : 8;
-    return w >= 8 ? 8 : 4;
+    const int w = e ? std::atoi(e) : 0;  // 0: per-stencil default
+    return w >= 8 ? 8 : (w >= 4 ? 4 : 0);
   }();
   return v;
 }
@@ -145,7 +146,7 @@ inline int cta_warps_3d() {
 inline int cta_strips_3d() {
   static const int v = [] {
     const char* e = std::getenv("SSAM_B200_3D_SX");
-    return e ? std::atoi(e) : 2;
+    return e ? std::atoi(e) : 0;  // 0: per-stencil default
   }();
   return v;
 }
@@ -181,6 +182,7 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   zsegs = std::max<long long>(1, std::min<long long>(zsegs, zrows));
   int zseg = static_cast<int>((zrows + zsegs - 1) / zsegs);
   zseg = std::max(zseg, std::min(zrows, 8 * (2 * K + 1)));
+  if (const char* zs = std::getenv("SSAM_B200_3D_ZSEG")) zseg = std::max(4, std::atoi(zs));
   p.zseg = zseg;
   p.z_begin = zb;
   p.z_end = ze;
@@ -192,8 +194,12 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
     // boxes halve the x-halo re-reads and make each row fetch ~1 KB
     // contiguous.  Box limits: 256 elements per dimension, shared memory.
     constexpr int DZ = kRing3D;
-    int wpb = cta_warps_3d();
-    int sx = (cta_strips_3d() >= 2 && lp.V + 32 * Q <= 256 && p.nstrips >= 2) ? 2 : 1;
+    // Measured defaults: the light 7-point star streams best from 2-strip x
+    // 4-row-group CTAs; heavier footprints from 1 x 4.
+    const bool light = std::is_same<Mask, StarMask3<1>>::value;
+    int wpb = cta_warps_3d() ? cta_warps_3d() : (light ? 8 : 4);
+    const int want_sx = cta_strips_3d() ? cta_strips_3d() : (light ? 2 : 1);
+    int sx = (want_sx >= 2 && lp.V + 32 * Q <= 256 && p.nstrips >= 2) ? 2 : 1;
     auto fits = [&](int w, int x) {
       const int yy = w / x;
       return yy * RY + 2 * K <= 256 && ring3d_bytes<T, Q, RY, K, DZ>(x, yy, lp.V) <= 200 * 1024;
