@@ -177,11 +177,12 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   p.ring = K;
   p.vec_ok = (a.nx % Q == 0) && aligned16(a.in) && aligned16(a.out);
   const int zrows = ze - zb;
-  const long long per_z = static_cast<long long>(p.nstrips) * p.ygroups;
-  long long zsegs = (static_cast<long long>(kSMs) * 48 + per_z - 1) / per_z;
-  zsegs = std::max<long long>(1, std::min<long long>(zsegs, zrows));
-  int zseg = static_cast<int>((zrows + zsegs - 1) / zsegs);
-  zseg = std::max(zseg, std::min(zrows, 8 * (2 * K + 1)));
+  // Short z-segments (measured: 608 -> 726 GCells/s for 3d7pt at 2048^2x514
+  // going from whole-z CTAs to 32 planes): many short CTAs keep the machine
+  // evenly loaded to the end and keep vertically adjacent CTAs in step, so
+  // their shared halo rows still hit in L2.  The 2K-plane prologue per
+  // segment is the price; SSAM_B200_3D_ZSEG overrides.
+  int zseg = std::min(zrows, 32 * std::max(1, K));
   if (const char* zs = std::getenv("SSAM_B200_3D_ZSEG")) zseg = std::max(4, std::atoi(zs));
   p.zseg = zseg;
   p.z_begin = zb;
