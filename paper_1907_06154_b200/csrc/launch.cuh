@@ -182,7 +182,10 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   // evenly loaded to the end and keep vertically adjacent CTAs in step, so
   // their shared halo rows still hit in L2.  The 2K-plane prologue per
   // segment is the price; SSAM_B200_3D_ZSEG overrides.
-  int zseg = std::min(zrows, 32 * std::max(1, K));
+  // Sweep at 2048^2 x 514 f32: 3d7pt best at 16-24 planes, the heavier
+  // poisson / 3d27pt / 3d13pt (compute-bound) at 48-64.
+  const bool light7 = std::is_same<Mask, StarMask3<1>>::value;
+  int zseg = std::min(zrows, light7 ? 24 : 32 * std::max(1, K) + 16);
   if (const char* zs = std::getenv("SSAM_B200_3D_ZSEG")) zseg = std::max(4, std::atoi(zs));
   p.zseg = zseg;
   p.z_begin = zb;
