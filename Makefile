@@ -34,6 +34,18 @@ $(LIB): $(CU_OBJS) $(CPP_OBJS)
 oracle:
 	$(MAKE) -C oracle
 
+# Debug variant: bounded mbarrier waits that report and trap (SSAM_DEBUG_HANG).
+# Load it with SSAM_B200_LIB=build/dbg/libssam_b200.so.
+DBG := build/dbg
+DBG_OBJS := $(patsubst $(SRC)/%.cu,$(DBG)/%.o,$(CU_SRCS))
+$(DBG)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(DBG)
+	$(NVCC) $(NVFLAGS) -DSSAM_DEBUG_HANG -c $< -o $@
+$(DBG)/libssam_b200.so: $(DBG_OBJS) $(CPP_OBJS)
+	$(NVCC) $(ARCH) -shared -cudart static -Xlinker -soname=libssam_b200.so $^ -o $@
+debug: $(DBG)/libssam_b200.so
+.PHONY: debug
+
 clean:
 	rm -rf $(BUILD) $(LIB)
 

@@ -33,7 +33,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libssam_b200.so")
+LIB_PATH = os.environ.get("SSAM_B200_LIB") or os.path.join(_HERE, "libssam_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 
 namespace ssam_b200 {
@@ -138,8 +139,20 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef SSAM_DEBUG_HANG
+  // debug builds (make debug): a wait that never completes reports and traps
+  long long n = 0;
+  while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1ll << 20)) {
+      printf("mbar_wait stuck: block (%d,%d,%d) thread %d bar 0x%x parity %u\n", blockIdx.x,
+             blockIdx.y, blockIdx.z, threadIdx.x, bar, parity);
+      __trap();
+    }
+  }
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 
 // 2D tiled TMA load of one box at element coordinates (x, y) of the tensor

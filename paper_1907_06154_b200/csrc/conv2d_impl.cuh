@@ -5,8 +5,10 @@
 // w[(m-1-j)*n + (n-1-t)]) and the boundary sampling of :23-28.
 #pragma once
 
+#include <cstdlib>
 #include <vector>
 
+#include "engine2d_fma.cuh"
 #include "launch.cuh"
 
 namespace ssam_b200 {
@@ -30,12 +32,96 @@ constexpr int conv_q(int n) {
   return sizeof(T) == 4 ? (n <= 4 ? 8 : 4) : 2;
 }
 
+// Square filters with K >= SSAM_B200_CONV_FMA (default 6; 0 = never) take the
+// FMA-bound engine (engine2d_fma.cuh).
+inline int conv_fma_min_k() {
+  static const int v = [] {
+    const char* e = std::getenv("SSAM_B200_CONV_FMA");
+    return e ? std::atoi(e) : 6;
+  }();
+  return v;
+}
+
+template <class T, int Q, int NR, int MC, int RY, bool EXACT, int CAP>
+cudaError_t launch_fma2d(const Engine2DArgs<T>& a, cudaStream_t s) {
+  constexpr int RB = RY > 4 ? RY : 4;
+  constexpr int D = 3;
+  if (a.M * NR > CAP || a.NR != NR || (MC > 0 && a.M != MC)) return cudaErrorInvalidValue;
+  if (a.y_end <= a.y_begin) return cudaSuccess;
+  Ssam2DTmaParams<T, CAP> P;
+  std::memset(&P, 0, sizeof(P));
+  Ssam2DParams<T, CAP>& p = P.p;
+  p.in = a.in;
+  p.out = a.out;
+  p.W = a.W;
+  p.H = a.H;
+  p.M = a.M;
+  if (EXACT) {
+    p.A = a.M - 1 - (a.M - 1) / 2;  // L: the box starts L columns left of the outputs
+    p.V = 32 * Q - (a.M - 1);
+  } else {
+    const LanePlan lp = plan_lanes(a.M, Q);
+    p.A = lp.A;
+    p.V = lp.V;
+  }
+  p.nstrips = (a.W + p.V - 1) / p.V;
+  const int rows = a.y_end - a.y_begin;
+  p.seg = (pick_seg(rows, p.nstrips, NR) + RB - 1) / RB * RB;
+  p.y_begin = a.y_begin;
+  p.y_end = a.y_end;
+  p.bmode = a.bmode;
+  p.ring = a.ring;
+  p.vec_ok = 1;
+  std::memcpy(p.coef, a.coef, sizeof(T) * a.M * NR);
+  auto kern = ssam2d_fma_kernel<T, Q, NR, MC, RY, RB, D, EXACT, CAP>;
+  const size_t smem = fma2d_smem<T, Q, NR, RB, D, EXACT>(kWarpsPerBlock, a.M);
+  const int gx = (p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  const dim3 grid(gx, (rows + p.seg - 1) / p.seg);
+  cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.W, a.H, sizeof(T) * a.W,
+                               fma2d_pitch<EXACT, Q>(), RB);
+  if (e != cudaSuccess) return e;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(P);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// TMA-eligible calls (zero boundary, 16-byte rows and pointers).
+template <class T>
+bool fma_eligible(const Engine2DArgs<T>& a) {
+  return a.bmode != kBndReplicate && a.W % (16 / sizeof(T)) == 0 && aligned16(a.in) &&
+         aligned16(a.out);
+}
+
+// Rows per pass (measured on B200, 8192^2 fp32, vs the light kernel):
+// RY = 4 up to 10x10 (+4..30%: shorter window shifts, 16 FMA chains),
+// RY = 2 at 11x11, RY = 1 beyond (the unrolled pass stays ~1600 FFMAs;
+// +3..10%).  The exact lane plan is used where it adds >= 1.5% columns.
+constexpr int fma_ry(int k) { return k <= 10 ? 4 : (k <= 11 ? 2 : 1); }
+constexpr bool fma_exact(int k, int q) {
+  const int r = (k - 1) / 2, l = k - 1 - r, a = (l + q - 1) / q * q;
+  const int v_aligned = (32 * q - r - a) / q * q, v_exact = 32 * q - (k - 1);
+  return fma_ry(k) == 1 && v_exact * 1000 >= v_aligned * 1015;
+}
+
+template <class T, int Q, int K>
+cudaError_t conv_fma_sq(const Engine2DArgs<T>& a, cudaStream_t s) {
+  return launch_fma2d<T, Q, K, K, fma_ry(K), fma_exact(K, Q), K * K>(a, s);
+}
+
 template <class T, int Q, int N>
 cudaError_t conv_rt(const Engine2DArgs<T>& a, cudaStream_t s) {
   return launch_ssam2d<T, Q, N, 0, DenseMask, pf_rows(N), 20 * N>(a, s);
 }
 template <class T, int Q, int K>
 cudaError_t conv_sq(const Engine2DArgs<T>& a, cudaStream_t s) {
+  if constexpr (K >= 3) {
+    const int kmin = conv_fma_min_k();
+    if (kmin > 0 && K >= kmin && fma_eligible(a)) return conv_fma_sq<T, Q == 8 ? 4 : Q, K>(a, s);
+  }
   return launch_ssam2d<T, Q, K, K, DenseMask, pf_rows(K), K * K>(a, s);
 }
 
