@@ -308,4 +308,246 @@ __global__ void __launch_bounds__(128) ssam3d_kernel(const __grid_constant__ Ssa
   }
 }
 
+
+// ===========================================================================
+// Full-warp lane plan with halo lanes (ssam3d_halo_kernel).
+//
+// The kernels above follow the paper's lane plan: a warp loads 32Q columns
+// and emits the ~32Q-2K whose chains stay inside the warp, rounded down to
+// whole Q-vectors (120 of 128 for K = 1).  On a 512-wide grid that is five
+// strips for 512 columns -- 15% of every load and FMA spent on columns
+// another warp also computes.  Here EVERY lane owns its Q columns (a warp
+// emits all 32Q) and the chain's missing inputs at the warp's two ends come
+// from halo lanes: lane 0 additionally holds the K columns left of the
+// strip, lane 31 the K columns right of it, read from a box that is VQ
+// columns wider on each side.  Each lane runs one short halo chain over
+// those K columns with its own coefficient set (lane 0: the left chain's
+// dx < 0 columns, lane 31: the mirrored right chain's dx > 0 columns --
+// the masks are x-symmetric) and the results are injected into the
+// systolic chain where shfl_up / shfl_down would have brought them in from
+// a lane outside the warp.  The injected sums are formed in exactly the
+// order the main chain uses (h_m(c) = h_{m-1}(c-1) + colpart_m(c), colpart
+// over (dz, dy) in the same tap order), so results are bit-identical to
+// the kernels above.
+// ===========================================================================
+
+// Window rows whose halo columns feed a dx != 0 tap (compile-time).
+template <int K, class Mask, int RY>
+__host__ __device__ constexpr bool halo_row_needed(int w) {
+  constexpr int M = 2 * K + 1;
+  for (int m = 0; m < K; ++m)
+    for (int l = 0; l < M; ++l)
+      for (int t = 0; t < M; ++t)
+        if (Mask::has(m, t, l) && w - t >= 0 && w - t < RY) return true;
+  return false;
+}
+
+// Shared memory of the halo kernel: DZ plane slots of sx per-strip boxes.
+template <class T, int Q, int RY, int K, int DZ>
+__host__ __device__ constexpr size_t halo3d_bytes(int sx, int sy) {
+  constexpr int VQ = 16 / sizeof(T);
+  return static_cast<size_t>(DZ) *
+             (sx * box_slot_elems<T>(sy * RY + 2 * K, 32 * Q + 2 * VQ) * sizeof(T) + 16) +
+         static_cast<size_t>(sx * sy) * 128;
+}
+
+// Two 256-thread CTAs per SM for the light fp32 star (fits 128 registers
+// without spills); heavier footprints keep their registers.
+template <class T, int K, class Mask>
+__host__ __device__ constexpr int halo3d_min_blocks() {
+  return (sizeof(T) == 4 && K == 1 && Mask::has(0, 1, 1) && !Mask::has(0, 0, 1)) ? 2 : 1;
+}
+
+template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP>
+__global__ void __launch_bounds__(256, (halo3d_min_blocks<T, K, Mask>()))
+    ssam3d_halo_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
+  static_assert(K >= 1, "order-0 stencils have no chain");
+  const Ssam3DParams<T, CAP>& p = P.p;
+  constexpr int M = 2 * K + 1;
+  constexpr int NROW = RY + 2 * K;
+  constexpr int NPL = M;
+  constexpr int VQ = 16 / sizeof(T);
+  constexpr int BW = 32 * Q + 2 * VQ;  // box width: the strip plus VQ columns each side
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  const int sx = p.cta_sx, sy = wpb / p.cta_sx;
+  const int wx = wib % sx, wy = wib / sx;
+  const int brows = sy * RY + 2 * K;
+  const uint32_t box_bytes = static_cast<uint32_t>(brows) * BW * sizeof(T);
+  const size_t sub_elems = box_slot_elems<T>(brows, BW);
+  const size_t slot_elems = sx * sub_elems;
+  const int y_cta0 = p.ring + blockIdx.y * sy * RY;
+  const int y_out0 = y_cta0 + wy * RY;
+  const int z0 = p.z_begin + blockIdx.z * p.zseg;
+  const int z1 = min(z0 + p.zseg, p.z_end);
+  const int x_cta0 = blockIdx.x * sx * 32 * Q;
+  const int x0 = x_cta0 + wx * 32 * Q + Q * lane;
+  const int count = (z1 - z0) + 2 * K;
+  const bool is_r = lane == 31;
+
+  // per-lane halo coefficients: lane 31 mirrors (dx -> -dx)
+  T hc[K][M][M];
+#pragma unroll
+  for (int m = 0; m < K; ++m)
+#pragma unroll
+    for (int l = 0; l < M; ++l)
+#pragma unroll
+      for (int t = 0; t < M; ++t)
+        hc[m][l][t] = Mask::has(m, t, l)
+                          ? (is_r ? p.coef[(l * M + (M - 1 - m)) * M + t] : p.coef[(l * M + m) * M + t])
+                          : T(0);
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + DZ * slot_elems * sizeof(T));
+  uint64_t* empty = full + DZ;
+  const uint32_t scratch = smem_u32(empty + DZ) + threadIdx.x * 4;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&P.tmap);
+#pragma unroll
+    for (int s = 0; s < DZ; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), wpb);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int i) {
+    const int s = i % DZ;
+    if (i >= DZ) mbar_wait(smem_u32(&empty[s]), ((i / DZ) - 1) & 1);
+    const uint32_t bar = smem_u32(&full[s]);
+    const int z = z0 - K + i;
+    const int row = (z >= 0 && z < p.nz) ? z * p.ny + (y_cta0 - K) : -brows;
+    mbar_arrive_expect_tx(bar, box_bytes * sx);
+    for (int w = 0; w < sx; ++w)
+      tma_load_2d(smem_u32(ring + s * slot_elems + w * sub_elems), &P.tmap,
+                  x_cta0 + w * 32 * Q - VQ, row, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < min(DZ, count); ++i) issue(i);
+  // halo column c of this lane: lane 0 -> x_strip0 - K + c, lane 31 -> x_strip_end + K - 1 - c
+  const int hoff0 = is_r ? VQ + 32 * Q + K - 1 : VQ - K;
+  const int hstep = is_r ? -1 : 1;
+  auto take = [&](int i, T (&dst)[NROW][Q], T (&hdst)[NROW][K]) {
+    const int s = i % DZ;
+    mbar_wait(smem_u32(&full[s]), (i / DZ) & 1);
+    const T* slot = ring + s * slot_elems + wx * sub_elems + static_cast<size_t>(wy * RY) * BW;
+#pragma unroll
+    for (int r = 0; r < NROW; ++r) lds_q<T, Q>(slot + r * BW + VQ + Q * lane, dst[r]);
+    uint32_t dep = 0;
+#pragma unroll
+    for (int r = 0; r < NROW; ++r) {
+      if (!halo_row_needed<K, Mask, RY>(r)) continue;
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        hdst[r][c] = slot[r * BW + hoff0 + hstep * c];
+        uint32_t bits;
+        memcpy(&bits, &hdst[r][c], sizeof(bits));
+        dep ^= bits;
+      }
+    }
+    wait_loaded<T, Q, NROW>(dst, 0, NROW, scratch);
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(scratch), "r"(dep) : "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+    if (threadIdx.x == 0 && i >= 1 && i - 1 + DZ < count) issue(i - 1 + DZ);
+  };
+
+  const int xlo = p.ring, xhi = p.nx - p.ring;
+  const int yhi = p.ny - p.ring;
+  const bool vec = x0 >= xlo && x0 + Q <= xhi;
+  T pl[NPL][NROW][Q];
+  T hp[NPL][NROW][K];
+#pragma unroll
+  for (int i = 0; i < NPL - 1; ++i) take(i, pl[i], hp[i]);
+  for (int zb = z0; zb < z1; zb += NPL) {
+#pragma unroll
+    for (int ph = 0; ph < NPL; ++ph) {
+      const int z = zb + ph;
+      if (z >= z1) break;
+      take(z - z0 + 2 * K, pl[(ph + NPL - 1) % NPL], hp[(ph + NPL - 1) % NPL]);
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        // halo chain: inj[m] = h_m(K-1), h_m(c) = h_{m-1}(c-1) + colpart_m(c)
+        T inj[K];
+        {
+          T h[K];
+#pragma unroll
+          for (int m = 0; m < K; ++m) {
+#pragma unroll
+            for (int c = K - 1; c >= m; --c) {
+              T cp = T(0);
+              bool any = false;
+#pragma unroll
+              for (int l = 0; l < M; ++l)
+#pragma unroll
+                for (int t = 0; t < M; ++t)
+                  if (Mask::has(m, t, l)) {
+                    const T v = hp[(ph + l) % NPL][r + t][c];
+                    cp = any ? fma_t(hc[m][l][t], v, cp) : hc[m][l][t] * v;
+                    any = true;
+                  }
+              if (m == 0)
+                h[c] = any ? cp : T(0);
+              else
+                h[c] = any ? h[c - 1] + cp : h[c - 1];
+            }
+            inj[m] = h[K - 1];
+          }
+        }
+        T acc[Q];
+#pragma unroll
+        for (int j = 0; j <= K; ++j) {
+          T cp[Q];
+          const bool any = colpart3<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, r, j, p, cp);
+          if (j == 0) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
+          } else {
+            shift_up1<T, Q>(acc);
+            if (lane == 0) acc[0] = inj[j - 1];
+            if (any) {
+#pragma unroll
+              for (int q = 0; q < Q; ++q) acc[q] += cp[q];
+            }
+          }
+        }
+        T accr[Q];
+#pragma unroll
+        for (int j = M - 1; j > K; --j) {
+          T cp[Q];
+          const bool any = colpart3<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, r, j, p, cp);
+          if (j == M - 1) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
+          } else {
+            shift_down1<T, Q>(accr);
+            if (is_r) accr[Q - 1] = inj[M - 2 - j];
+            if (any) {
+#pragma unroll
+              for (int q = 0; q < Q; ++q) accr[q] += cp[q];
+            }
+          }
+        }
+        shift_down1<T, Q>(accr);
+        if (is_r) accr[Q - 1] = inj[K - 1];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[q] += accr[q];
+        const int y = y_out0 + r;
+        if (y < yhi) {
+          T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
+          if (vec) {
+            st_q<T, Q>(row, acc);
+          } else {
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+              if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc[q];
+          }
+        }
+      }
+    }
+  }
+}
+
 }  // namespace ssam_b200

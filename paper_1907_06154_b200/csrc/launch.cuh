@@ -151,6 +151,25 @@ inline int cta_strips_3d() {
   return v;
 }
 
+// The halo-lane 3D kernel (engine3d.cuh) exists for order >= 1 x-symmetric
+// masks except the 125-tap box.  Measured (B200, 512^3 and 2048^2x514, vs
+// the aligned-plan kernel, bit-identical): fp32 3d7pt +12% / +1.3%, 3d13pt
+// fp32 +22%, fp64 +8%; the 27-point box, Poisson and fp64 3d7pt lose
+// 3-17% (their extra halo registers cost occupancy), so they keep the
+// aligned plan.  SSAM_B200_3D_HALO=0/1 forces it off/on where it exists.
+inline int halo_mode_3d() {
+  static const int v = [] {
+    const char* e = std::getenv("SSAM_B200_3D_HALO");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+template <class T, int K, class Mask>
+constexpr bool halo_default_3d() {
+  return std::is_same<Mask, StarMask3<2>>::value ||
+         (sizeof(T) == 4 && std::is_same<Mask, StarMask3<1>>::value);
+}
+
 template <class T, int Q, int K, class Mask, int RY, int CAP>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
@@ -191,7 +210,47 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   p.z_begin = zb;
   p.z_end = ze;
   std::memcpy(p.coef, a.coef, sizeof(T) * M * M * M);
-  if (tma) {
+  bool launched = false;
+  if constexpr (K >= 1 && !(K >= 2 && std::is_same<Mask, DenseMask3>::value)) {
+    const int hm = halo_mode_3d();
+    if (tma && (hm > 0 || (hm < 0 && halo_default_3d<T, K, Mask>()))) {
+      // Full-warp lane plan with halo lanes (ssam3d_halo_kernel): every warp
+      // emits 32Q columns; CTA = sx strips x sy row groups, one box per strip.
+      constexpr int DZ = kRing3D;
+      constexpr int VQ = 16 / sizeof(T);
+      p.A = 0;
+      p.V = 32 * Q;
+      p.nstrips = (a.nx - K + p.V - 1) / p.V;
+      const bool light = std::is_same<Mask, StarMask3<1>>::value;
+      int wpb = cta_warps_3d() ? cta_warps_3d() : (light ? 8 : 4);
+      const int want_sx = cta_strips_3d() ? cta_strips_3d() : (light ? 2 : 1);
+      int sx = (want_sx >= 2 && p.nstrips >= 2) ? 2 : 1;
+      auto fits = [&](int w, int x) {
+        const int yy = w / x;
+        return yy * RY + 2 * K <= 256 && halo3d_bytes<T, Q, RY, K, DZ>(x, yy) <= 200 * 1024;
+      };
+      while (wpb > sx * 2 && !fits(wpb, sx)) wpb /= 2;
+      const int sy = wpb / sx;
+      p.cta_sx = sx;
+      const dim3 grid((p.nstrips + sx - 1) / sx, (p.ygroups + sy - 1) / sy,
+                      (zrows + zseg - 1) / zseg);
+      cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
+                                   static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx,
+                                   32 * Q + 2 * VQ, sy * RY + 2 * K);
+      if (e != cudaSuccess) return e;
+      auto kern = ssam3d_halo_kernel<T, Q, K, Mask, RY, DZ, CAP>;
+      const size_t smem = halo3d_bytes<T, Q, RY, K, DZ>(sx, sy);
+      if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      kern<<<grid, 32 * wpb, smem, s>>>(P);
+      launched = true;
+    }
+  }
+  if (launched) {
+    // halo kernel above
+  } else if (tma) {
     // Taller CTAs share more of the y halo (2K rows per wpb*RY); the box
     // must stay within TMA's 256-row limit and the ring within shared memory.
     // CTA = sx adjacent strips x sy row groups sharing one plane box: wider
