@@ -34,17 +34,22 @@ $(LIB): $(CU_OBJS) $(CPP_OBJS)
 oracle:
 	$(MAKE) -C oracle
 
-# Debug variant: bounded mbarrier waits that report and trap (SSAM_DEBUG_HANG).
-# Load it with SSAM_B200_LIB=build/dbg/libssam_b200.so.
-DBG := build/dbg
-DBG_OBJS := $(patsubst $(SRC)/%.cu,$(DBG)/%.o,$(CU_SRCS))
-$(DBG)/%.o: $(SRC)/%.cu $(HDRS)
-	@mkdir -p $(DBG)
-	$(NVCC) $(NVFLAGS) -DSSAM_DEBUG_HANG -c $< -o $@
-$(DBG)/libssam_b200.so: $(DBG_OBJS) $(CPP_OBJS)
+# Variant builds for A/B experiments: make variant VAR=name VFLAGS="-D..." ->
+# build/var_name/libssam_b200.so (load with SSAM_B200_LIB=...).  `make debug`
+# is the variant with bounded mbarrier waits that report and trap.
+VAR ?= dbg
+VFLAGS ?= -DSSAM_DEBUG_HANG
+VDIR := build/var_$(VAR)
+V_OBJS := $(patsubst $(SRC)/%.cu,$(VDIR)/%.o,$(CU_SRCS))
+$(VDIR)/%.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(VDIR)
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $< -o $@
+$(VDIR)/libssam_b200.so: $(V_OBJS) $(CPP_OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -Xlinker -soname=libssam_b200.so $^ -o $@
-debug: $(DBG)/libssam_b200.so
-.PHONY: debug
+variant: $(VDIR)/libssam_b200.so
+debug:
+	$(MAKE) variant VAR=dbg VFLAGS=-DSSAM_DEBUG_HANG
+.PHONY: variant debug
 
 clean:
 	rm -rf $(BUILD) $(LIB)

@@ -170,7 +170,7 @@ constexpr bool halo_default_3d() {
          (sizeof(T) == 4 && std::is_same<Mask, StarMask3<1>>::value);
 }
 
-template <class T, int Q, int K, class Mask, int RY, int CAP>
+template <class T, int Q, int K, class Mask, int RY, int CAP, int RYH = RY>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
   static_assert(M * M * M <= CAP, "coefficient capacity");
@@ -227,19 +227,20 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
       int sx = (want_sx >= 2 && p.nstrips >= 2) ? 2 : 1;
       auto fits = [&](int w, int x) {
         const int yy = w / x;
-        return yy * RY + 2 * K <= 256 && halo3d_bytes<T, Q, RY, K, DZ>(x, yy) <= 200 * 1024;
+        return yy * RYH + 2 * K <= 256 && halo3d_bytes<T, Q, RYH, K, DZ>(x, yy) <= 200 * 1024;
       };
       while (wpb > sx * 2 && !fits(wpb, sx)) wpb /= 2;
       const int sy = wpb / sx;
       p.cta_sx = sx;
+      p.ygroups = (yrows + RYH - 1) / RYH;
       const dim3 grid((p.nstrips + sx - 1) / sx, (p.ygroups + sy - 1) / sy,
                       (zrows + zseg - 1) / zseg);
       cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
                                    static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx,
-                                   32 * Q + 2 * VQ, sy * RY + 2 * K);
+                                   32 * Q + 2 * VQ, sy * RYH + 2 * K);
       if (e != cudaSuccess) return e;
-      auto kern = ssam3d_halo_kernel<T, Q, K, Mask, RY, DZ, CAP>;
-      const size_t smem = halo3d_bytes<T, Q, RY, K, DZ>(sx, sy);
+      auto kern = ssam3d_halo_kernel<T, Q, K, Mask, RYH, DZ, CAP>;
+      const size_t smem = halo3d_bytes<T, Q, RYH, K, DZ>(sx, sy);
       if (smem > 48 * 1024) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
