@@ -317,7 +317,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": f"ssam3d_tma_kernel {STENCIL} f32",
+                         "kernel": f"ssam3d_halo_kernel {STENCIL} f32",
                          "bytes_per_launch": 8 * cells_per_launch,
                          "mean_launch_ms": round(mean_ms, 4)},
             "e2e": e2e, "gpu_launches": int(nl.item()), "clocks": clk,

@@ -73,6 +73,8 @@ class Oracle:
         lib.ssam_oracle_benchmark_stencil.argtypes = [C.c_char_p, C.POINTER(_i), C.POINTER(_i),
                                                       C.POINTER(_i), _p, _p, _i]
         lib.ssam_oracle_benchmark_name.restype = C.c_char_p
+        lib.ssam_oracle_conv1d.argtypes = [_i, _p, _i, _p, _i, _i, _p]
+        lib.ssam_oracle_scan.argtypes = [_i, _p, C.c_size_t, _p]
         self.lib = lib
 
     # -- generators (grid.hpp:52-66, filter.hpp:41-47) --------------------
@@ -119,6 +121,23 @@ class Oracle:
         assert rc == 0
         return out
 
+    def conv1d(self, signal: np.ndarray, filt: np.ndarray, boundary: int = 0) -> np.ndarray:
+        """oracle::conv1d_naive (oracle.hpp:61-73)."""
+        g = np.ascontiguousarray(signal)
+        f = np.ascontiguousarray(filt, dtype=g.dtype)
+        out = np.empty_like(g)
+        rc = self.lib.ssam_oracle_conv1d(dtype_code(g.dtype), _ptr(g), g.size, _ptr(f), f.size,
+                                         boundary, _ptr(out))
+        assert rc == 0
+        return out
+
+    def scan(self, values: np.ndarray) -> np.ndarray:
+        """oracle::scan_naive (oracle.hpp:118-127)."""
+        g = np.ascontiguousarray(values)
+        out = np.empty_like(g)
+        assert self.lib.ssam_oracle_scan(dtype_code(g.dtype), _ptr(g), g.size, _ptr(out)) == 0
+        return out
+
     # -- stencil_catalog.cpp ------------------------------------------------
     def benchmark_names(self):
         n = self.lib.ssam_oracle_benchmark_count()
@@ -154,6 +173,8 @@ class Reference:
         lib.ssam_ref_random_filter.argtypes = [_i, _p, _i, _i, _u64]
         lib.ssam_ref_benchmark_stencil.argtypes = [C.c_char_p, C.POINTER(_i), C.POINTER(_i),
                                                    C.POINTER(_i), _p, _p, _i]
+        lib.ssam_ref_conv1d.argtypes = [_i, _p, _i, _p, _i, _i, _i, _p, _p, _i]
+        lib.ssam_ref_scan.argtypes = [_i, _p, _i, _i, _p, _p, _i]
         self.lib = lib
 
     def max_threads(self) -> int:
@@ -218,6 +239,25 @@ class Reference:
         rc = self.lib.ssam_ref_stencil3d(dtype_code(g.dtype), _ptr(g), nx, ny, nz, dims, order,
                                          _ptr(off), _ptr(cf), off.shape[0], p, b, lane_count,
                                          threads, iters, _ptr(out), _ptr(cnt), int(naive))
+        return rc, out, cnt
+
+    def conv1d(self, signal, filt, *, boundary=0, lane_count=32, naive=False):
+        """ssam::conv1d (kernels.hpp:390-418) or oracle::conv1d_naive -> (status, out, counters)."""
+        g = np.ascontiguousarray(signal)
+        f = np.ascontiguousarray(filt, dtype=g.dtype)
+        out = np.zeros_like(g)
+        cnt = np.zeros(5, dtype=np.uint64)
+        rc = self.lib.ssam_ref_conv1d(dtype_code(g.dtype), _ptr(g), g.size, _ptr(f), f.size,
+                                      boundary, lane_count, _ptr(out), _ptr(cnt), int(naive))
+        return rc, out, cnt
+
+    def scan(self, values, *, lane_count=32, naive=False):
+        """ssam::scan (kernels.hpp:422-447) or oracle::scan_naive -> (status, out, counters)."""
+        g = np.ascontiguousarray(values)
+        out = np.zeros_like(g)
+        cnt = np.zeros(5, dtype=np.uint64)
+        rc = self.lib.ssam_ref_scan(dtype_code(g.dtype), _ptr(g), g.size, lane_count, _ptr(out),
+                                    _ptr(cnt), int(naive))
         return rc, out, cnt
 
 

@@ -125,6 +125,33 @@ int stencil3d_t(const void* in, int nx, int ny, int nz, const Stencil<T>& st,
   });
 }
 
+template <class T>
+int conv1d_t(const void* in, int len, const void* wts, int m, const KernelConfig& cfg, void* out,
+             std::uint64_t* counters, bool naive) {
+  return guarded([&] {
+    const T* ip = static_cast<const T*>(in);
+    const T* wp = static_cast<const T*>(wts);
+    std::vector<T> sig(ip, ip + len), f(wp, wp + m);
+    OpCounters c;
+    std::vector<T> r = naive ? oracle::conv1d_naive(sig, f, cfg.boundary) : conv1d(sig, f, cfg, &c);
+    std::memcpy(out, r.data(), sizeof(T) * r.size());
+    put_counters(c, counters);
+  });
+}
+
+template <class T>
+int scan_t(const void* in, int len, int lane_count, void* out, std::uint64_t* counters,
+           bool naive) {
+  return guarded([&] {
+    const T* ip = static_cast<const T*>(in);
+    std::vector<T> v(ip, ip + len);
+    OpCounters c;
+    std::vector<T> r = naive ? oracle::scan_naive(v) : scan(v, lane_count, &c);
+    if (!r.empty()) std::memcpy(out, r.data(), sizeof(T) * r.size());
+    put_counters(c, counters);
+  });
+}
+
 }  // namespace
 
 extern "C" {
@@ -233,6 +260,27 @@ int ssam_ref_benchmark_stencil(const char* name, int* dims, int* order, int* fpp
   } catch (...) {
     return -1;
   }
+}
+
+int ssam_ref_conv1d(int dtype, const void* in, int len, const void* wts, int m, int boundary,
+                    int lane_count, void* out, std::uint64_t* counters, int naive) {
+  const KernelConfig cfg = make_cfg(4, 128, boundary, lane_count, 0);
+  switch (dtype) {
+    case F32: return conv1d_t<float>(in, len, wts, m, cfg, out, counters, naive != 0);
+    case F64: return conv1d_t<double>(in, len, wts, m, cfg, out, counters, naive != 0);
+    case I64: return conv1d_t<long long>(in, len, wts, m, cfg, out, counters, naive != 0);
+  }
+  return 1;
+}
+
+int ssam_ref_scan(int dtype, const void* in, int len, int lane_count, void* out,
+                  std::uint64_t* counters, int naive) {
+  switch (dtype) {
+    case F32: return scan_t<float>(in, len, lane_count, out, counters, naive != 0);
+    case F64: return scan_t<double>(in, len, lane_count, out, counters, naive != 0);
+    case I64: return scan_t<long long>(in, len, lane_count, out, counters, naive != 0);
+  }
+  return 1;
 }
 
 }  // extern "C"

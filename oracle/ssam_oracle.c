@@ -19,6 +19,8 @@
  *   conv2d_naive .......... proj/include/ssam/oracle.hpp:44-59 (double acc for FP, s-major then t)
  *   stencil2d_naive ....... proj/include/ssam/oracle.hpp:80-96 (Jacobi, ring of width k fixed)
  *   stencil3d_naive ....... proj/include/ssam/oracle.hpp:98-116
+ *   conv1d_naive .......... proj/include/ssam/oracle.hpp:61-73 (sample1d :30-36)
+ *   scan_naive ............ proj/include/ssam/oracle.hpp:118-127
  *   benchmark catalog ..... proj/src/stencil_catalog.cpp:21-112
  *
  * Accumulation: double for f32/f64 inputs, native int64 for i64, one rounding
@@ -121,6 +123,62 @@ int ssam_oracle_conv2d(int dtype, const void* in, int w, int h, const void* wts,
     case SSAM_F32: CONV2D_BODY(float, double) break;
     case SSAM_F64: CONV2D_BODY(double, double) break;
     case SSAM_I64: CONV2D_BODY(int64_t, int64_t) break;
+    default: return 1;
+  }
+  return 0;
+}
+
+/* oracle.hpp:61-73: out(i) = sum_{s<m} in(i+ax-s) * f[s], ax = (m-1)/2,
+ * sample1d (:30-36) zero or clamp-replicate. */
+#define CONV1D_BODY(T, ACC)                                                  \
+  {                                                                          \
+    const T* g = (const T*)in;                                               \
+    const T* f = (const T*)wts;                                              \
+    T* o = (T*)out;                                                          \
+    const int ax = (m - 1) / 2;                                              \
+    for (int i = 0; i < len; ++i) {                                          \
+      ACC sum = 0;                                                           \
+      for (int s = 0; s < m; ++s) {                                          \
+        int j = i + ax - s;                                                  \
+        T v;                                                                 \
+        if (j >= 0 && j < len) v = g[j];                                     \
+        else if (boundary == 0) v = (T)0;                                    \
+        else v = g[clampi(j, len)];                                          \
+        sum += (ACC)v * (ACC)f[s];                                           \
+      }                                                                      \
+      o[i] = (T)sum;                                                         \
+    }                                                                        \
+  }
+
+int ssam_oracle_conv1d(int dtype, const void* in, int len, const void* wts, int m, int boundary,
+                       void* out) {
+  if (len < 0 || m < 1) return 1;
+  switch (dtype) {
+    case SSAM_F32: CONV1D_BODY(float, double) break;
+    case SSAM_F64: CONV1D_BODY(double, double) break;
+    case SSAM_I64: CONV1D_BODY(int64_t, int64_t) break;
+    default: return 1;
+  }
+  return 0;
+}
+
+/* oracle.hpp:118-127: running sum in Acc<T>, rounded to T per element. */
+#define SCAN_BODY(T, ACC)                                                    \
+  {                                                                          \
+    const T* g = (const T*)in;                                               \
+    T* o = (T*)out;                                                          \
+    ACC run = 0;                                                             \
+    for (size_t i = 0; i < len; ++i) {                                       \
+      run += (ACC)g[i];                                                      \
+      o[i] = (T)run;                                                         \
+    }                                                                        \
+  }
+
+int ssam_oracle_scan(int dtype, const void* in, size_t len, void* out) {
+  switch (dtype) {
+    case SSAM_F32: SCAN_BODY(float, double) break;
+    case SSAM_F64: SCAN_BODY(double, double) break;
+    case SSAM_I64: SCAN_BODY(int64_t, int64_t) break;
     default: return 1;
   }
   return 0;

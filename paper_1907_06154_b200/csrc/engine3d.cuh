@@ -37,6 +37,7 @@ struct Ssam3DParams {
   int ring;         // = K
   int vec_ok;
   int cta_sx;       // TMA kernel: adjacent x-strips per CTA (sharing one box)
+  int zfast;        // TMA kernels: grid is (x, z-segment, y-group) instead of (x, y, z)
   T coef[CAP];      // coef[(l*M + j)*M + t], l = dz+K, j = dx+K, t = dy+K
 };
 
@@ -211,9 +212,9 @@ __global__ void __launch_bounds__(256)
   const int bcols = (sx - 1) * p.V + ROW;
   const uint32_t box_bytes = static_cast<uint32_t>(brows) * bcols * sizeof(T);
   const size_t slot_elems = box_slot_elems<T>(brows, bcols);
-  const int y_cta0 = p.ring + blockIdx.y * sy * RY;
+  const int y_cta0 = p.ring + (p.zfast ? blockIdx.z : blockIdx.y) * sy * RY;
   const int y_out0 = y_cta0 + wy * RY;
-  const int z0 = p.z_begin + blockIdx.z * p.zseg;
+  const int z0 = p.z_begin + (p.zfast ? blockIdx.y : blockIdx.z) * p.zseg;
   const int z1 = min(z0 + p.zseg, p.z_end);
   const int base = blockIdx.x * sx * p.V - p.A;  // box origin (16-byte aligned)
   const int x_out0 = (blockIdx.x * sx + wx) * p.V;
@@ -377,9 +378,9 @@ __global__ void __launch_bounds__(256, (halo3d_min_blocks<T, K, Mask>()))
   const uint32_t box_bytes = static_cast<uint32_t>(brows) * BW * sizeof(T);
   const size_t sub_elems = box_slot_elems<T>(brows, BW);
   const size_t slot_elems = sx * sub_elems;
-  const int y_cta0 = p.ring + blockIdx.y * sy * RY;
+  const int y_cta0 = p.ring + (p.zfast ? blockIdx.z : blockIdx.y) * sy * RY;
   const int y_out0 = y_cta0 + wy * RY;
-  const int z0 = p.z_begin + blockIdx.z * p.zseg;
+  const int z0 = p.z_begin + (p.zfast ? blockIdx.y : blockIdx.z) * p.zseg;
   const int z1 = min(z0 + p.zseg, p.z_end);
   const int x_cta0 = blockIdx.x * sx * 32 * Q;
   const int x0 = x_cta0 + wx * 32 * Q + Q * lane;

@@ -72,6 +72,16 @@ template <class T>
 cudaError_t stencil3d_direct(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin,
                              int z_end, const StencilDesc<T>& st, cudaStream_t s);
 
+// ---- 1D: conv1d and scan (kernels.hpp:390-447) -------------------------------
+// conv1d: out(i) = sum_{s<m} in(i + (m-1)/2 - s) * w[s], m <= 32 (the
+// reference's lane_count cap), boundary zero or replicate.
+template <class T>
+cudaError_t conv1d_device(const T* d_in, T* d_out, int len, const T* h_w, int m, int boundary,
+                          cudaStream_t s);
+// Inclusive prefix sum of n elements (one pass, decoupled look-back).
+template <class T>
+cudaError_t scan_device(const T* d_in, T* d_out, size_t n, cudaStream_t s);
+
 // ---- utilities --------------------------------------------------------------
 cudaError_t fill_random(int dtype, void* d, std::size_t count, std::uint64_t seed,
                         std::uint64_t first, cudaStream_t s);

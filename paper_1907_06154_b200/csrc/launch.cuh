@@ -55,6 +55,7 @@ struct Engine2DArgs {
   const T* coef;  // host, [M][NR]
   int bmode, ring;
   int y_begin, y_end;
+  bool direct = false;  // force the direct-load kernel (1-row grids: conv1d)
 };
 
 // Taps of a compile-time footprint (MC == 0: runtime width, count as dense 20).
@@ -79,7 +80,7 @@ cudaError_t launch_ssam2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   if (a.M * NR > CAP || a.NR != NR || (MC > 0 && a.M != MC)) return cudaErrorInvalidValue;
   if (a.y_end <= a.y_begin) return cudaSuccess;
   constexpr int VQ = 16 / sizeof(T);
-  const bool tma = a.bmode != kBndReplicate && a.W % VQ == 0 && aligned16(a.in) &&
+  const bool tma = !a.direct && a.bmode != kBndReplicate && a.W % VQ == 0 && aligned16(a.in) &&
                    aligned16(a.out);
   Ssam2DTmaParams<T, CAP> P;
   std::memset(&P, 0, sizeof(P));
@@ -170,6 +171,26 @@ constexpr bool halo_default_3d() {
          (sizeof(T) == 4 && std::is_same<Mask, StarMask3<1>>::value);
 }
 
+// CTA order of the TMA kernels.  The hardware launches blockIdx.x fastest,
+// then y, then z.  (x, y-group, z-segment) re-reads each segment's 2K halo
+// planes long after the neighbouring segment read them (HBM, not L2);
+// (x, z-segment, y-group) makes z-neighbours concurrent instead.  Measured on
+// B200 the second order is SLOWER everywhere (3d7pt 2048^2x514: 774 -> 718
+// GCells/s; 512^3 cases -3..6%), so (x, y, z) stays the default;
+// SSAM_B200_3D_ZFAST=1 selects the other.
+inline int zfast_3d() {
+  static const int v = [] {
+    const char* e = std::getenv("SSAM_B200_3D_ZFAST");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+template <class P3>
+dim3 grid3d(P3& p, int gx, int gy, int gz) {
+  p.zfast = zfast_3d() != 0 && gz <= 65535;
+  return p.zfast ? dim3(gx, gz, gy) : dim3(gx, gy, gz);
+}
+
 template <class T, int Q, int K, class Mask, int RY, int CAP, int RYH = RY>
 cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
@@ -233,8 +254,8 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
       const int sy = wpb / sx;
       p.cta_sx = sx;
       p.ygroups = (yrows + RYH - 1) / RYH;
-      const dim3 grid((p.nstrips + sx - 1) / sx, (p.ygroups + sy - 1) / sy,
-                      (zrows + zseg - 1) / zseg);
+      const dim3 grid = grid3d(p, (p.nstrips + sx - 1) / sx, (p.ygroups + sy - 1) / sy,
+                               (zrows + zseg - 1) / zseg);
       cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
                                    static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx,
                                    32 * Q + 2 * VQ, sy * RYH + 2 * K);
@@ -271,8 +292,8 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
     while (wpb > sx * 2 && !fits(wpb, sx)) wpb /= 2;
     const int sy = wpb / sx;
     p.cta_sx = sx;
-    const dim3 grid((p.nstrips + sx - 1) / sx, (p.ygroups + sy - 1) / sy,
-                    (zrows + zseg - 1) / zseg);
+    const dim3 grid = grid3d(p, (p.nstrips + sx - 1) / sx, (p.ygroups + sy - 1) / sy,
+                             (zrows + zseg - 1) / zseg);
     cudaError_t e = make_tmap_2d(&P.tmap, a.in, sizeof(T), a.nx,
                                  static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx,
                                  (sx - 1) * lp.V + 32 * Q, sy * RY + 2 * K);
