@@ -12,7 +12,13 @@
  *   Grid3D<T> stencil3d(const Grid3D<T>&, const Stencil<T>&, const KernelConfig&,
  *                       int iters, OpCounters* = nullptr);                 // kernels.hpp:283
  *
- * with T in {float, double, long long} (proj/tools/ssam_cli.cpp:241-243).
+ * with T in {float, double, long long} (proj/tools/ssam_cli.cpp:241-243), and the
+ * 1D entry points of the same header:
+ *
+ *   std::vector<T> conv1d(const std::vector<T>&, const std::vector<T>&,
+ *                         const KernelConfig&, OpCounters* = nullptr);  // kernels.hpp:390
+ *   std::vector<T> scan  (const std::vector<T>&, int lane_count = 32,
+ *                         OpCounters* = nullptr);                       // kernels.hpp:422
  * Each entry point below replaces one of them; include/ssam_b200/kernels.hpp
  * re-exposes the exact C++ signatures on top of this ABI and re-raises the
  * reference's exception types from the status codes.
@@ -36,7 +42,7 @@
 extern "C" {
 #endif
 
-#define SSAM_B200_ABI_VERSION 1
+#define SSAM_B200_ABI_VERSION 2
 
 /* Element type of a call: float, double, long long (int64). */
 typedef enum { SSAM_DTYPE_F32 = 0, SSAM_DTYPE_F64 = 1, SSAM_DTYPE_I64 = 2 } ssam_dtype;
@@ -185,6 +191,27 @@ int ssam_b200_fill_random(int dtype, void* d_out, size_t count, uint64_t seed, u
  * reduced on the device; synchronises the stream. */
 int ssam_b200_max_rel_err(int dtype, const void* d_a, const void* d_b, size_t count,
                           double* max_rel, double* max_abs, void* stream);
+
+/* ---- 1D: conv1d and scan (replace kernels.hpp:390 / :422) ----------------
+ * conv1d: out(i) = sum_{s<m} in(i + (m-1)/2 - s) * w[s] (oracle.hpp:61-73),
+ * cfg->boundary zero or replicate; the reference's checks: m in
+ * [1, lane_count], len >= lane_count, lane_count a power of two in [2, 64]
+ * (all std::invalid_argument).  scan: inclusive prefix sum; len must be a
+ * multiple of lane_count (empty input is returned as is).  Host buffers,
+ * synchronous; counters accumulate the simulator's tallies. */
+int ssam_b200_conv1d(int dtype, const void* in, long long len, const void* weights, int m,
+                     const ssam_kernel_config* cfg, void* out, ssam_op_counters* counters);
+int ssam_b200_scan(int dtype, const void* in, unsigned long long len, int lane_count, void* out,
+                   ssam_op_counters* counters);
+int ssam_b200_check_conv1d(long long len, int m, const ssam_kernel_config* cfg);
+int ssam_b200_check_scan(unsigned long long len, int lane_count);
+int ssam_b200_counters_conv1d(long long len, int m, const ssam_kernel_config* cfg,
+                              ssam_op_counters* counters);
+int ssam_b200_counters_scan(unsigned long long len, int lane_count, ssam_op_counters* counters);
+/* Device-resident, stream-ordered: conv1d (m <= 32) and a one-pass scan. */
+int ssam_b200_conv1d_device(int dtype, const void* d_in, void* d_out, int len,
+                            const void* h_weights, int m, int boundary, void* stream);
+int ssam_b200_scan_device(int dtype, const void* d_in, void* d_out, size_t len, void* stream);
 
 #ifdef __cplusplus
 }

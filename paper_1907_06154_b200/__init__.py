@@ -123,6 +123,15 @@ _sig("ssam_b200_stencil3d_run", [_i, _p, _p, _i, _i, _i, _PS, _i, _p, C.POINTER(
 _sig("ssam_b200_fill_random", [_i, _p, _sz, _u64, _u64, _p])
 _sig("ssam_b200_max_rel_err", [_i, _p, _p, _sz, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                _p])
+_ll, _ull = C.c_longlong, C.c_ulonglong
+_sig("ssam_b200_conv1d", [_i, _p, _ll, _p, _i, _PC, _p, _PK])
+_sig("ssam_b200_scan", [_i, _p, _ull, _i, _p, _PK])
+_sig("ssam_b200_check_conv1d", [_ll, _i, _PC])
+_sig("ssam_b200_check_scan", [_ull, _i])
+_sig("ssam_b200_counters_conv1d", [_ll, _i, _PC, _PK])
+_sig("ssam_b200_counters_scan", [_ull, _i, _PK])
+_sig("ssam_b200_conv1d_device", [_i, _p, _p, _i, _p, _i, _i, _p])
+_sig("ssam_b200_scan_device", [_i, _p, _p, _sz, _p])
 
 lib = _lib  # raw handle for device-level callers (bench.py, tests)
 
@@ -136,7 +145,9 @@ EXPORTED = [
     "ssam_b200_benchmark_name", "ssam_b200_benchmark_stencil", "ssam_b200_conv2d_device",
     "ssam_b200_stencil2d_sweep", "ssam_b200_stencil2d_tb", "ssam_b200_stencil2d_tb_max",
     "ssam_b200_stencil3d_sweep", "ssam_b200_stencil2d_run", "ssam_b200_stencil3d_run",
-    "ssam_b200_fill_random", "ssam_b200_max_rel_err",
+    "ssam_b200_fill_random", "ssam_b200_max_rel_err", "ssam_b200_conv1d", "ssam_b200_scan",
+    "ssam_b200_check_conv1d", "ssam_b200_check_scan", "ssam_b200_counters_conv1d",
+    "ssam_b200_counters_scan", "ssam_b200_conv1d_device", "ssam_b200_scan_device",
 ]
 
 
@@ -393,7 +404,73 @@ def stencil3d(grid: np.ndarray, st: Stencil, cfg: Optional[KernelConfig] = None,
     return out
 
 
+def _vector(a) -> np.ndarray:
+    a = np.asarray(a)
+    if a.ndim != 1:
+        raise InvalidArgument(f"expected a 1D signal, got shape {a.shape}")
+    if a.dtype not in _DT:
+        raise InvalidArgument(f"unsupported dtype {a.dtype}; use float32, float64 or int64")
+    return np.ascontiguousarray(a)
+
+
+def conv1d(signal, filt, cfg: Optional[KernelConfig] = None,
+           counters: Optional[OpCounters] = None) -> np.ndarray:
+    """ssam::conv1d (kernels.hpp:390-418): out(i) = sum_s in(i + (m-1)/2 - s) f[s]
+    with cfg.boundary; m in [1, lane_count], len >= lane_count."""
+    g = _vector(signal)
+    f = np.ascontiguousarray(np.asarray(filt).astype(g.dtype, copy=False).reshape(-1))
+    cfg = cfg or KernelConfig()
+    out = np.empty_like(g)
+    cnt = counters._load() if counters is not None else None
+    st = _lib.ssam_b200_conv1d(_DT[g.dtype], g.ctypes.data, g.size, f.ctypes.data, f.size,
+                               C.byref(cfg._c()), out.ctypes.data,
+                               C.byref(cnt) if cnt is not None else None)
+    _raise(st)
+    if counters is not None:
+        counters._store(cnt)
+    return out
+
+
+def scan(values, lane_count: int = 32, counters: Optional[OpCounters] = None) -> np.ndarray:
+    """ssam::scan (kernels.hpp:422-447): inclusive prefix sum; the length must be a
+    multiple of lane_count."""
+    g = _vector(values)
+    out = np.empty_like(g)
+    cnt = counters._load() if counters is not None else None
+    st = _lib.ssam_b200_scan(_DT[g.dtype], g.ctypes.data, g.size, lane_count, out.ctypes.data,
+                             C.byref(cnt) if cnt is not None else None)
+    _raise(st)
+    if counters is not None:
+        counters._store(cnt)
+    return out
+
+
 # -- validation / counters without a device ----------------------------------
+
+def check_conv1d(length: int, m: int, cfg: Optional[KernelConfig] = None) -> None:
+    _raise(_lib.ssam_b200_check_conv1d(length, m, C.byref((cfg or KernelConfig())._c())))
+
+
+def check_scan(length: int, lane_count: int = 32) -> None:
+    _raise(_lib.ssam_b200_check_scan(length, lane_count))
+
+
+def counters_conv1d(length: int, m: int, cfg=None) -> OpCounters:
+    c = _Counters()
+    _raise(_lib.ssam_b200_counters_conv1d(length, m, C.byref((cfg or KernelConfig())._c()),
+                                          C.byref(c)))
+    o = OpCounters()
+    o._store(c)
+    return o
+
+
+def counters_scan(length: int, lane_count: int = 32) -> OpCounters:
+    c = _Counters()
+    _raise(_lib.ssam_b200_counters_scan(length, lane_count, C.byref(c)))
+    o = OpCounters()
+    o._store(c)
+    return o
+
 
 def check_conv2d(w: int, h: int, m: int, n: int, cfg: Optional[KernelConfig] = None) -> None:
     _raise(_lib.ssam_b200_check_conv2d(w, h, m, n, C.byref((cfg or KernelConfig())._c())))

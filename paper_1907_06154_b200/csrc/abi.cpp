@@ -471,6 +471,104 @@ template <class T> struct HostStencil {
   template <class... A> static int run(A... a) { return host_stencil<T>(a...); }
 };
 
+// ---- 1D: conv1d / scan (kernels.hpp:390-447) -----------------------------------
+bool pow2_lanes(int s) { return s >= 2 && s <= 64 && (s & (s - 1)) == 0; }
+
+// ssam::conv1d's checks in its order (kernels.hpp:393-397, then the
+// WarpState constructor, warp.hpp:36-38, on the first tile).
+int check_conv1d(long long len, int m, const ssam_kernel_config& c) {
+  const int s = c.lane_count;
+  if (m < 1 || m > s)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "conv1d: filter length must be in [1, lane_count]");
+  if (len < s) return fail(SSAM_ERR_INVALID_ARGUMENT, "conv1d: signal shorter than one warp");
+  if (!pow2_lanes(s))
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "warp: lane_count must be a power of two in [2, 64]");
+  return SSAM_OK;
+}
+
+// ssam::scan's checks (kernels.hpp:425-429, make_scan_plan plan.hpp:199-201).
+// An empty input returns before the plan is built, so any lane_count > 0 is
+// accepted for it; lane_count <= 0 (undefined in the reference) is rejected.
+int check_scan(unsigned long long len, int s) {
+  if (s <= 0) return fail(SSAM_ERR_INVALID_ARGUMENT, "scan: lane_count must be positive");
+  if (len % static_cast<unsigned long long>(s) != 0)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "scan: length must be a multiple of lane_count");
+  if (len == 0) return SSAM_OK;
+  if (!pow2_lanes(s))
+    return fail(SSAM_ERR_INVALID_ARGUMENT,
+                "scan plan: lane_count must be a power of two in [2, 64]");
+  return SSAM_OK;
+}
+
+// Closed forms of the simulator's counts: conv1d tiles of valid_w = S-m+1
+// outputs, each m MAD stages (broadcast weight), m-1 shifts, S loads;
+// scan tiles of S, each log2(S) MAD + shuffle stages (immediate 1), S loads
+// and S stores.
+void counters_conv1d(long long len, int m, const ssam_kernel_config& c, ssam_op_counters* o) {
+  const std::uint64_t s = c.lane_count;
+  const std::uint64_t tiles = ceil_div(static_cast<std::uint64_t>(len), s - m + 1);
+  o->mads += tiles * m;
+  o->shuffles += tiles * (m - 1);
+  o->broadcast_reads += tiles * m;
+  o->global_loads += tiles * s;
+  o->global_stores += static_cast<std::uint64_t>(len);
+}
+void counters_scan(unsigned long long len, int s, ssam_op_counters* o) {
+  if (len == 0) return;
+  const std::uint64_t tiles = len / s;
+  std::uint64_t lg = 0;
+  while ((1 << lg) < s) ++lg;
+  o->mads += tiles * lg;
+  o->shuffles += tiles * lg;
+  o->global_loads += len;
+  o->global_stores += len;
+}
+
+template <class T>
+int host_conv1d(const void* in, int len, const void* wts, int m, int boundary, void* out) {
+  cudaStream_t s = cudaStreamPerThread;
+  const size_t bytes = static_cast<size_t>(len) * sizeof(T);
+  DevBuf din(s), dout(s);
+  cudaError_t e;
+  if ((e = din.alloc(bytes)) != cudaSuccess) return cuda_fail(e, "conv1d alloc");
+  if ((e = dout.alloc(bytes)) != cudaSuccess) return cuda_fail(e, "conv1d alloc");
+  if ((e = cudaMemcpyAsync(din.p, in, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "conv1d H2D");
+  if ((e = conv1d_device<T>(static_cast<const T*>(din.p), static_cast<T*>(dout.p), len,
+                            static_cast<const T*>(wts), m, boundary, s)) != cudaSuccess)
+    return cuda_fail(e, "conv1d kernel");
+  if ((e = cudaMemcpyAsync(out, dout.p, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "conv1d D2H");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "conv1d sync");
+  return SSAM_OK;
+}
+
+template <class T>
+int host_scan(const void* in, size_t len, void* out) {
+  cudaStream_t s = cudaStreamPerThread;
+  const size_t bytes = len * sizeof(T);
+  DevBuf din(s), dout(s);
+  cudaError_t e;
+  if ((e = din.alloc(bytes)) != cudaSuccess) return cuda_fail(e, "scan alloc");
+  if ((e = dout.alloc(bytes)) != cudaSuccess) return cuda_fail(e, "scan alloc");
+  if ((e = cudaMemcpyAsync(din.p, in, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "scan H2D");
+  if ((e = scan_device<T>(static_cast<const T*>(din.p), static_cast<T*>(dout.p), len, s)) !=
+      cudaSuccess)
+    return cuda_fail(e, "scan kernel");
+  if ((e = cudaMemcpyAsync(out, dout.p, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "scan D2H");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "scan sync");
+  return SSAM_OK;
+}
+
+template <class T> struct HostConv1 {
+  template <class... A> static int run(A... a) { return host_conv1d<T>(a...); }
+};
+template <class T> struct HostScan {
+  template <class... A> static int run(A... a) { return host_scan<T>(a...); }
+};
+
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
@@ -767,6 +865,86 @@ int ssam_b200_max_rel_err(int dtype, const void* d_a, const void* d_b, size_t co
   if (max_rel) *max_rel = r;
   if (max_abs) *max_abs = a;
   return SSAM_OK;
+}
+
+// ---- 1D entry points (kernels.hpp:390-447) ----------------------------------------
+int ssam_b200_check_conv1d(long long len, int m, const ssam_kernel_config* cfg) {
+  g_err.clear();
+  return check_conv1d(len, m, cfg_or_default(cfg));
+}
+int ssam_b200_check_scan(unsigned long long len, int lane_count) {
+  g_err.clear();
+  return check_scan(len, lane_count);
+}
+int ssam_b200_counters_conv1d(long long len, int m, const ssam_kernel_config* cfg,
+                              ssam_op_counters* counters) {
+  const ssam_kernel_config c = cfg_or_default(cfg);
+  if (int s = check_conv1d(len, m, c)) return s;
+  if (counters) counters_conv1d(len, m, c, counters);
+  return SSAM_OK;
+}
+int ssam_b200_counters_scan(unsigned long long len, int lane_count, ssam_op_counters* counters) {
+  if (int s = check_scan(len, lane_count)) return s;
+  if (counters) counters_scan(len, lane_count, counters);
+  return SSAM_OK;
+}
+
+int ssam_b200_conv1d(int dtype, const void* in, long long len, const void* weights, int m,
+                     const ssam_kernel_config* cfg, void* out, ssam_op_counters* counters) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  const ssam_kernel_config c = cfg_or_default(cfg);
+  if (int s = check_conv1d(len, m, c)) return s;
+  if (len > 0x7fffffffLL) return fail(SSAM_ERR_INVALID_ARGUMENT, "conv1d: signal too long");
+  if (!in || !out || !weights) return fail(SSAM_ERR_INVALID_ARGUMENT, "conv1d: null pointer");
+  if (int s = device_ready()) return s;
+  const int b = c.boundary == SSAM_BOUNDARY_REPLICATE ? 1 : 0;
+  if (int s = by_dtype<HostConv1>(dtype, in, static_cast<int>(len), weights, m, b, out)) return s;
+  if (counters) counters_conv1d(len, m, c, counters);
+  return SSAM_OK;
+}
+
+int ssam_b200_scan(int dtype, const void* in, unsigned long long len, int lane_count, void* out,
+                   ssam_op_counters* counters) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = check_scan(len, lane_count)) return s;
+  if (len == 0) return SSAM_OK;
+  if (!in || !out) return fail(SSAM_ERR_INVALID_ARGUMENT, "scan: null pointer");
+  if (int s = device_ready()) return s;
+  if (int s = by_dtype<HostScan>(dtype, in, static_cast<size_t>(len), out)) return s;
+  if (counters) counters_scan(len, lane_count, counters);
+  return SSAM_OK;
+}
+
+int ssam_b200_conv1d_device(int dtype, const void* d_in, void* d_out, int len,
+                            const void* h_weights, int m, int boundary, void* stream) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (m < 1 || m > 32 || len < 0) return fail(SSAM_ERR_INVALID_ARGUMENT, "conv1d_device: bad shape");
+  if (int s = device_ready()) return s;
+  cudaError_t e = cudaErrorInvalidValue;
+  const cudaStream_t s = as_stream(stream);
+  switch (dtype) {
+    case 0: e = conv1d_device<float>(static_cast<const float*>(d_in), static_cast<float*>(d_out), len, static_cast<const float*>(h_weights), m, boundary, s); break;
+    case 1: e = conv1d_device<double>(static_cast<const double*>(d_in), static_cast<double*>(d_out), len, static_cast<const double*>(h_weights), m, boundary, s); break;
+    case 2: e = conv1d_device<long long>(static_cast<const long long*>(d_in), static_cast<long long*>(d_out), len, static_cast<const long long*>(h_weights), m, boundary, s); break;
+  }
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "conv1d_device");
+}
+
+int ssam_b200_scan_device(int dtype, const void* d_in, void* d_out, size_t len, void* stream) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = device_ready()) return s;
+  cudaError_t e = cudaErrorInvalidValue;
+  const cudaStream_t s = as_stream(stream);
+  switch (dtype) {
+    case 0: e = scan_device<float>(static_cast<const float*>(d_in), static_cast<float*>(d_out), len, s); break;
+    case 1: e = scan_device<double>(static_cast<const double*>(d_in), static_cast<double*>(d_out), len, s); break;
+    case 2: e = scan_device<long long>(static_cast<const long long*>(d_in), static_cast<long long*>(d_out), len, s); break;
+  }
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "scan_device");
 }
 
 }  // extern "C"

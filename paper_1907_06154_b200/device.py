@@ -118,3 +118,18 @@ def max_rel_err(a, b, stream=None) -> Tuple[float, float]:
     _raise(_lib.ssam_b200_max_rel_err(_code(a), a.data_ptr(), b.data_ptr(), a.numel(),
                                       C.byref(rel), C.byref(ab), _s(stream)))
     return rel.value, ab.value
+
+
+def conv1d(d_in, d_out, weights, boundary: int = 0, stream=None) -> None:
+    """conv1d of a 1D device signal (m <= 32)."""
+    code = _code(d_in)
+    w = np.ascontiguousarray(np.asarray(weights).astype(_np_dtype(code)).reshape(-1))
+    _raise(_lib.ssam_b200_conv1d_device(code, d_in.data_ptr(), d_out.data_ptr(), d_in.numel(),
+                                        w.ctypes.data, w.size, int(boundary), _s(stream)))
+
+
+def scan(d_in, d_out, stream=None) -> None:
+    """Inclusive prefix sum of a device tensor (flattened)."""
+    code = _code(d_in)
+    _raise(_lib.ssam_b200_scan_device(code, d_in.data_ptr(), d_out.data_ptr(), d_in.numel(),
+                                      _s(stream)))

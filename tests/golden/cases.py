@@ -11,6 +11,8 @@ Sources of the case lists (relative to /root/reference):
   CONV_UNIT_SHAPES ...... proj/tests/test_kernels_conv.cpp:47-48
   stencil cases ......... proj/tests/acceptance.cpp:76-114 (criterion 2),
                           proj/tests/test_kernels_stencil.cpp:59-106, 155-185
+  conv1d / scan cases ... proj/tests/test_kernels_conv.cpp:136-187, :210-221,
+                          proj/tests/acceptance.cpp:116-135 (criterion 3)
 """
 from __future__ import annotations
 
@@ -69,4 +71,29 @@ def stencil3d_cases():
         cases.append((f"{name}_f64", "f64", 64, 64, 64, name, 13, 2))
         cases.append((f"{name}_f32", "f32", 64, 64, 64, name, 13, 2))
     cases.append(("int3d", "i64", 36, 10, 9, None, 31, 2))
+    return cases
+
+
+def conv1d_cases():
+    """(tag, dtype, len, m, signal_seed, filter_seed, boundary, lane_count).
+    Signal = random_grid stream of `len`, filter = random_filter(m, 1)."""
+    cases = []
+    for bnd in (0, 1):
+        for m in (1, 2, 3, 9, 32):
+            cases.append((f"i64_211_m{m}_b{bnd}", "i64", 211, m, 8 + m, 80 + m, bnd, 32))
+        for m in (5, 16):
+            cases.append((f"f32_4099_m{m}_b{bnd}", "f32", 4099, m, 3, 4, bnd, 32))
+            cases.append((f"f64_4099_m{m}_b{bnd}", "f64", 4099, m, 3, 4, bnd, 32))
+    cases.append(("i64_48_m7_l16", "i64", 48, 7, 5, 6, 0, 16))
+    return cases
+
+
+def scan_cases():
+    """(tag, dtype, len, seed, lane_count)."""
+    cases = []
+    for tiles in (1, 3, 7, 128):
+        cases.append((f"i64_t{tiles}", "i64", 32 * tiles, 55 + tiles, 32))
+    cases.append(("i64_l16", "i64", 48, 9, 16))
+    cases.append(("f64_4096", "f64", 4096, 2, 32))
+    cases.append(("f32_4096", "f32", 4096, 2, 32))
     return cases

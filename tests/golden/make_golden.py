@@ -42,7 +42,7 @@ def main() -> None:
     ref = Reference()
     out: dict = {"generator": "tests/golden/make_golden.py", "reference": "/root/reference/proj",
                  "rng": {}, "filters": {}, "catalog": {}, "conv": {}, "stencil2d": {},
-                 "stencil3d": {}}
+                 "stencil3d": {}, "conv1d": {}, "scan": {}}
 
     for dt in ("f32", "f64", "i64"):
         for seed in (0, 1, 11, 13, 1234, 4321):
@@ -99,6 +99,23 @@ def main() -> None:
         assert rc == 0, (tag, rc)
         out["stencil3d"][tag] = dict(oracle=digest(want), ssam=digest(got), counters=cnt.tolist(),
                                      p=2, b=b)
+
+    for tag, dt, n, m, ss, fs, bnd, lanes in C.conv1d_cases():
+        sig = ref.random_grid(n, NP[dt], ss)
+        f = ref.random_filter(m, 1, NP[dt], fs).reshape(-1)
+        rc, want, _ = ref.conv1d(sig, f, boundary=bnd, lane_count=lanes, naive=True)
+        assert rc == 0
+        rc, got, cnt = ref.conv1d(sig, f, boundary=bnd, lane_count=lanes)
+        assert rc == 0, (tag, rc)
+        out["conv1d"][tag] = dict(oracle=digest(want), ssam=digest(got), counters=cnt.tolist())
+
+    for tag, dt, n, seed, lanes in C.scan_cases():
+        v = ref.random_grid(n, NP[dt], seed)
+        rc, want, _ = ref.scan(v, lane_count=lanes, naive=True)
+        assert rc == 0
+        rc, got, cnt = ref.scan(v, lane_count=lanes)
+        assert rc == 0, (tag, rc)
+        out["scan"][tag] = dict(oracle=digest(want), ssam=digest(got), counters=cnt.tolist())
 
     path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden.json")
     with open(path, "w") as fh:

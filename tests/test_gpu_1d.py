@@ -1,0 +1,111 @@
+"""conv1d and scan on the GPU vs the oracle (run with -m gpu on a B200).
+
+Mirrors proj/tests/test_kernels_conv.cpp:136-187, :210-221 and acceptance
+criterion 3 (proj/tests/acceptance.cpp:116-135: 1000 random int64 scans of
+1..127 tiles, exact).  Tolerances (ssam_cli.cpp:48-55): int64 bit-exact,
+f64 <= 1e-12, f32 <= 1e-5 as max |got-want| / max(1, |want|).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import cases as C
+from oracle import max_rel_err
+
+pytestmark = pytest.mark.gpu
+NP = {"f32": np.float32, "f64": np.float64, "i64": np.int64}
+TOL = {"f32": 1e-5, "f64": 1e-12, "i64": 0.0}
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_conv1d_identity_and_box(cuda_lib):
+    ramp = np.arange(100, dtype=np.int64)
+    assert np.array_equal(cuda_lib.conv1d(ramp, [1]), ramp)
+    out = cuda_lib.conv1d(ramp, np.ones(5, np.int64))
+    assert all(out[i] == 5 * i for i in range(2, 98))
+
+
+def test_conv1d_golden(cuda_lib, orc, golden):
+    for tag, dt, n, m, ss, fs, bnd, lanes in C.conv1d_cases():
+        sig = orc.random_grid(n, NP[dt], ss)
+        f = orc.random_filter(m, 1, NP[dt], fs).reshape(-1)
+        cnt = cuda_lib.OpCounters()
+        got = cuda_lib.conv1d(sig, f, cuda_lib.KernelConfig(boundary=cuda_lib.Boundary(bnd),
+                                                            lane_count=lanes), cnt)
+        if dt == "i64":
+            assert digest(got) == golden["conv1d"][tag]["oracle"], tag
+        else:
+            assert max_rel_err(got, orc.conv1d(sig, f, bnd)) <= TOL[dt], tag
+        assert list(cnt.as_tuple()) == golden["conv1d"][tag]["counters"], tag
+
+
+def test_conv1d_random_vs_oracle(cuda_lib, orc):
+    rng = np.random.default_rng(8)
+    for dt in ("i64", "f32", "f64"):
+        for _ in range(20):
+            m = int(rng.integers(1, 33))
+            n = int(rng.integers(32, 5000))
+            bnd = int(rng.integers(0, 2))
+            sig = orc.random_grid(n, NP[dt], int(rng.integers(1 << 40)))
+            f = orc.random_filter(m, 1, NP[dt], int(rng.integers(1 << 40))).reshape(-1)
+            got = cuda_lib.conv1d(sig, f, cuda_lib.KernelConfig(boundary=cuda_lib.Boundary(bnd)))
+            assert max_rel_err(got, orc.conv1d(sig, f, bnd)) <= TOL[dt], (dt, n, m, bnd)
+
+
+def test_conv1d_large(cuda_lib, orc):
+    n = (1 << 22) + 3
+    sig = orc.random_grid(n, np.float32, 1)
+    f = orc.random_filter(9, 1, np.float32, 2).reshape(-1)
+    assert max_rel_err(cuda_lib.conv1d(sig, f), orc.conv1d(sig, f, 0)) <= 1e-5
+
+
+def test_scan_reference_cases(cuda_lib, orc):
+    cnt = cuda_lib.OpCounters()
+    out = cuda_lib.scan(np.ones(96, np.int64), 32, cnt)
+    assert out.tolist() == list(range(1, 97))
+    assert cnt.shuffles == 15
+    alt = np.array([1 if i % 2 == 0 else -1 for i in range(64)], np.int64)
+    assert cuda_lib.scan(alt).tolist() == [1 if i % 2 == 0 else 0 for i in range(64)]
+    assert cuda_lib.scan(np.zeros(0, np.int64)).size == 0
+    with pytest.raises(cuda_lib.InvalidArgument):
+        cuda_lib.scan(np.ones(33, np.int64))
+    v = np.random.default_rng(9).integers(-50, 50, 48).astype(np.int64)
+    cnt = cuda_lib.OpCounters()
+    assert np.array_equal(cuda_lib.scan(v, 16, cnt), orc.scan(v))
+    assert cnt.shuffles == 12
+
+
+def test_scan_golden(cuda_lib, orc, golden):
+    for tag, dt, n, seed, lanes in C.scan_cases():
+        v = orc.random_grid(n, NP[dt], seed)
+        got = cuda_lib.scan(v, lanes)
+        if dt == "i64":
+            assert digest(got) == golden["scan"][tag]["oracle"], tag
+        else:
+            assert max_rel_err(got, orc.scan(v)) <= TOL[dt], tag
+
+
+def test_scan_criterion3_property(cuda_lib, orc):
+    """acceptance.cpp:116-135: 1000 random int64 inputs of 1..127 tiles, exact."""
+    rng = np.random.default_rng(100)
+    for _ in range(1000):
+        tiles = int(rng.integers(1, 128))
+        v = rng.integers(-1000000, 1000001, 32 * tiles).astype(np.int64)
+        assert np.array_equal(cuda_lib.scan(v), orc.scan(v)), tiles
+
+
+def test_scan_large_multi_tile(cuda_lib, orc):
+    """Many look-back tiles: 2^24 + 32 elements (int64 exact, f64 / f32 within tolerance)."""
+    n = (1 << 24) + 32
+    v = np.random.default_rng(3).integers(-1 << 20, 1 << 20, n).astype(np.int64)
+    assert np.array_equal(cuda_lib.scan(v), orc.scan(v))
+    x = orc.random_grid(n, np.float64, 4)
+    assert max_rel_err(cuda_lib.scan(x), orc.scan(x)) <= 1e-12
+    # fp32 prefix sums lose ~sqrt(tiles) ulps of |S| along the tile chain; 2^20
+    # elements keep the hybrid error metric well inside 1e-5
+    x = orc.random_grid(1 << 20, np.float32, 4)
+    assert max_rel_err(cuda_lib.scan(x), orc.scan(x)) <= 1e-5
