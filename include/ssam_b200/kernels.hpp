@@ -155,4 +155,36 @@ Grid3D<T> stencil3d(const Grid3D<T>& in, const Stencil<T>& st, const KernelConfi
   return out;
 }
 
+// kernels.hpp:390 -- 1D convolution out(i) = sum_s in(i + (m-1)/2 - s) * f[s].
+template <class T>
+std::vector<T> conv1d(const std::vector<T>& signal, const std::vector<T>& filter,
+                      const KernelConfig& cfg, OpCounters* counters = nullptr) {
+  const ssam_kernel_config c = b200_detail::to_c(cfg);
+  const long long len = static_cast<long long>(signal.size());
+  const int m = static_cast<int>(filter.size());
+  b200_detail::check(ssam_b200_check_conv1d(len, m, &c));
+  std::vector<T> out(signal.size());
+  ssam_op_counters oc = b200_detail::to_c(counters);
+  b200_detail::check(ssam_b200_conv1d(b200_detail::Dtype<T>::value, signal.data(), len,
+                                      filter.data(), m, &c, out.data(),
+                                      counters ? &oc : nullptr));
+  b200_detail::from_c(oc, counters);
+  return out;
+}
+
+// kernels.hpp:422 -- inclusive prefix sum in lane_count tiles.
+template <class T>
+std::vector<T> scan(const std::vector<T>& values, int lane_count = 32,
+                    OpCounters* counters = nullptr) {
+  const unsigned long long len = values.size();
+  b200_detail::check(ssam_b200_check_scan(len, lane_count));
+  if (values.empty()) return {};
+  std::vector<T> out(values.size());
+  ssam_op_counters oc = b200_detail::to_c(counters);
+  b200_detail::check(ssam_b200_scan(b200_detail::Dtype<T>::value, values.data(), len, lane_count,
+                                    out.data(), counters ? &oc : nullptr));
+  b200_detail::from_c(oc, counters);
+  return out;
+}
+
 }  // namespace ssam

@@ -288,6 +288,76 @@ int main() {
     }
   });
 
+  // ---- proj/tests/test_kernels_conv.cpp:136-187, :210-221; acceptance criterion 3 ----
+  run("conv1d identity, box-on-ramp, and oracle equality", [] {
+    std::vector<long long> ramp(100);
+    for (int i = 0; i < 100; ++i) ramp[i] = i;
+    KernelConfig cfg;
+    std::vector<long long> ident = {1};
+    CHECK(conv1d(ramp, ident, cfg) == ramp);
+    std::vector<long long> box(5, 1);
+    auto out = conv1d(ramp, box, cfg);
+    for (int i = 2; i < 98; ++i) CHECK(out[i] == 5 * i);
+    SplitMix64 rng(8);
+    for (int m : {2, 3, 9, 32}) {
+      std::vector<long long> f(m), sig(211);
+      for (auto& v : f) v = rng.next_int(-9, 9);
+      for (auto& v : sig) v = rng.next_int(-100, 100);
+      CHECK(conv1d(sig, f, cfg) == oracle::conv1d_naive(sig, f, Boundary::zero));
+      KernelConfig repl = cfg;
+      repl.boundary = Boundary::replicate;
+      CHECK(conv1d(sig, f, repl) == oracle::conv1d_naive(sig, f, Boundary::replicate));
+    }
+    std::vector<long long> shorty(10, 1);
+    CHECK(throws<std::invalid_argument>([&] { conv1d(shorty, box, cfg); }));
+    std::vector<long long> wide(33, 1);
+    CHECK(throws<std::invalid_argument>([&] { conv1d(ramp, wide, cfg); }));
+  });
+
+  run("scan matches prefix sums and uses 5 shuffles per 32-lane tile", [] {
+    std::vector<long long> ones(96, 1);
+    OpCounters counters;
+    auto out = scan(ones, 32, &counters);
+    for (int i = 0; i < 96; ++i) CHECK(out[i] == i + 1);
+    CHECK(counters.shuffles == 3 * 5);
+    std::vector<long long> alt(64);
+    for (int i = 0; i < 64; ++i) alt[i] = i % 2 == 0 ? 1 : -1;
+    auto alt_out = scan(alt);
+    for (int i = 0; i < 64; ++i) CHECK(alt_out[i] == (i % 2 == 0 ? 1 : 0));
+    SplitMix64 rng(55);
+    for (int tiles : {1, 3, 7}) {
+      std::vector<long long> v(32 * tiles);
+      for (auto& x : v) x = rng.next_int(-1000, 1000);
+      CHECK(scan(v) == oracle::scan_naive(v));
+    }
+    std::vector<long long> ragged(33, 1);
+    CHECK(throws<std::invalid_argument>([&] { scan(ragged); }));
+    CHECK(scan(std::vector<long long>{}).empty());
+  });
+
+  run("scan at lane_count 16", [] {
+    std::vector<long long> v(48);
+    SplitMix64 rng(9);
+    for (auto& x : v) x = rng.next_int(-50, 50);
+    OpCounters counters;
+    CHECK(scan(v, 16, &counters) == oracle::scan_naive(v));
+    CHECK(counters.shuffles == 3 * 4);
+  });
+
+  run("acceptance: scan-prefix-sums", [] {
+    SplitMix64 rng(100);
+    for (int rep = 0; rep < 1000; ++rep) {
+      const int tiles = static_cast<int>(rng.next_int(1, 128));
+      std::vector<long long> v(static_cast<std::size_t>(tiles) * 32);
+      for (auto& x : v) x = rng.next_int(-1000000, 1000000);
+      CHECK(scan(v) == oracle::scan_naive(v));
+    }
+    OpCounters counters;
+    std::vector<long long> one_tile(32, 3);
+    scan(one_tile, 32, &counters);
+    CHECK(counters.shuffles == 5);
+  });
+
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

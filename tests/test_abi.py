@@ -26,7 +26,7 @@ def test_header_and_exports_agree(lib):
 
 
 def test_abi_version(lib):
-    assert lib.lib.ssam_b200_abi_version() == 1
+    assert lib.lib.ssam_b200_abi_version() == 2
 
 
 def test_default_config_matches_reference(lib):
