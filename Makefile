@@ -15,7 +15,7 @@ CXXFLAGS := -std=c++17 -O2 -fPIC -Wall -Iinclude -I$(SRC) -I$(CUDA_HOME)/include
 
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
-CPP_OBJS := $(BUILD)/abi.o $(BUILD)/tmap.o
+CPP_OBJS := $(BUILD)/abi.o $(BUILD)/tmap.o $(BUILD)/grid_io.o
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp) include/ssam_b200.h
 
 all: $(LIB) oracle dropin
@@ -55,6 +55,10 @@ clean:
 	rm -rf $(BUILD) $(LIB)
 
 .PHONY: all oracle clean
+
+$(BUILD)/grid_io.o: $(SRC)/grid_io.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
 
 $(BUILD)/tmap.o: $(SRC)/tmap.cpp $(HDRS)
 	@mkdir -p $(BUILD)

@@ -56,7 +56,8 @@ typedef enum {
   SSAM_ERR_LENGTH = 2,           /* the reference throws std::length_error (C > 255) */
   SSAM_ERR_CUDA = 3,             /* CUDA runtime failure; see ssam_b200_last_error() */
   SSAM_ERR_NO_DEVICE = 4,        /* no usable CUDA device */
-  SSAM_ERR_OUT_OF_MEMORY = 5     /* device allocation failed */
+  SSAM_ERR_OUT_OF_MEMORY = 5,    /* device allocation failed */
+  SSAM_ERR_RUNTIME = 6           /* the reference throws std::runtime_error (grid I/O) */
 } ssam_status;
 
 /* ssam::KernelConfig (filter.hpp:117-139).  Validated exactly like
@@ -212,6 +213,21 @@ int ssam_b200_counters_scan(unsigned long long len, int lane_count, ssam_op_coun
 int ssam_b200_conv1d_device(int dtype, const void* d_in, void* d_out, int len,
                             const void* h_weights, int m, int boundary, void* stream);
 int ssam_b200_scan_device(int dtype, const void* d_in, void* d_out, size_t len, void* stream);
+
+/* ---- SGRD grid files (proj/include/ssam/grid_io.hpp:14-158) ---------------
+ * The reference's binary format: "SGRD", version 1, rank, scalar code
+ * (f32 1 / f64 2 / i64 3), u16 dims (d0 fastest, unused = 1), raw
+ * little-endian scalars.  dims > 65535 -> SSAM_ERR_INVALID_ARGUMENT; bad
+ * magic, version, rank or scalar type, truncation and unopenable files ->
+ * SSAM_ERR_RUNTIME (std::runtime_error in the reference).  on_device != 0:
+ * the buffer is device memory and the payload streams through pinned
+ * staging buffers on `stream` (disk I/O overlapped with the PCIe copies);
+ * both calls return when the data has landed. */
+int ssam_b200_sgrd_info(const char* path, int* rank, int* dtype, int* dims /* [3] */);
+int ssam_b200_sgrd_read(const char* path, int dtype, int rank, int* dims /* [3], out */, void* dst,
+                        size_t capacity_elems, int on_device, void* stream);
+int ssam_b200_sgrd_write(const char* path, int dtype, int rank, const int* dims /* [3] */,
+                         const void* src, int on_device, void* stream);
 
 #ifdef __cplusplus
 }

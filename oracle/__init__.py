@@ -175,6 +175,8 @@ class Reference:
                                                    C.POINTER(_i), _p, _p, _i]
         lib.ssam_ref_conv1d.argtypes = [_i, _p, _i, _p, _i, _i, _i, _p, _p, _i]
         lib.ssam_ref_scan.argtypes = [_i, _p, _i, _i, _p, _p, _i]
+        lib.ssam_ref_sgrd_write.argtypes = [_i, C.c_char_p, _i, _p, _p]
+        lib.ssam_ref_sgrd_read.argtypes = [_i, C.c_char_p, _i, _p, _p, C.c_longlong]
         self.lib = lib
 
     def max_threads(self) -> int:
@@ -259,6 +261,24 @@ class Reference:
         rc = self.lib.ssam_ref_scan(dtype_code(g.dtype), _ptr(g), g.size, lane_count, _ptr(out),
                                     _ptr(cnt), int(naive))
         return rc, out, cnt
+
+    def sgrd_write(self, path: str, a: np.ndarray) -> int:
+        """ssam::write_grid_file (grid_io.hpp:129-134); rank = a.ndim, dims x-fastest."""
+        a = np.ascontiguousarray(a)
+        dims = np.array(list(a.shape[::-1]) + [1] * (3 - a.ndim), dtype=np.int32)
+        return self.lib.ssam_ref_sgrd_write(dtype_code(a.dtype), path.encode(), a.ndim,
+                                            _ptr(dims), _ptr(a))
+
+    def sgrd_read(self, path: str, dtype, rank: int, cap: int = 1 << 24):
+        """read_vector / read_grid2d / read_grid3d -> (status, array or None)."""
+        dims = np.zeros(3, dtype=np.int32)
+        buf = np.zeros(cap, dtype=dtype)
+        rc = self.lib.ssam_ref_sgrd_read(dtype_code(dtype), path.encode(), rank, _ptr(dims),
+                                         _ptr(buf), cap)
+        if rc != 0:
+            return rc, None
+        shape = tuple(int(d) for d in dims[:rank][::-1])
+        return 0, buf[:int(np.prod(shape))].reshape(shape).copy()
 
 
 def max_rel_err(got: np.ndarray, want: np.ndarray) -> float:

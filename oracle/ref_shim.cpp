@@ -27,6 +27,7 @@
 #include "ssam/grid.hpp"
 #include "ssam/kernels.hpp"
 #include "ssam/oracle.hpp"
+#include "ssam/grid_io.hpp"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -47,6 +48,8 @@ int guarded(Fn&& fn) {
     return 2;
   } catch (const std::invalid_argument&) {
     return 1;
+  } catch (const std::runtime_error&) {
+    return 3;
   } catch (...) {
     return 9;
   }
@@ -149,6 +152,45 @@ int scan_t(const void* in, int len, int lane_count, void* out, std::uint64_t* co
     std::vector<T> r = naive ? oracle::scan_naive(v) : scan(v, lane_count, &c);
     if (!r.empty()) std::memcpy(out, r.data(), sizeof(T) * r.size());
     put_counters(c, counters);
+  });
+}
+
+// SGRD files through the reference's own writer / readers (grid_io.hpp).
+template <class T>
+int sgrd_write_t(const char* path, int rank, const int* dims, const void* data) {
+  return guarded([&] {
+    const T* p = static_cast<const T*>(data);
+    if (rank == 1) {
+      write_grid_file<T>(path, std::vector<T>(p, p + dims[0]));
+    } else if (rank == 2) {
+      Grid2D<T> g(dims[0], dims[1]);
+      std::memcpy(g.data.data(), p, sizeof(T) * g.data.size());
+      write_grid_file<T>(path, g);
+    } else {
+      Grid3D<T> g(dims[0], dims[1], dims[2]);
+      std::memcpy(g.data.data(), p, sizeof(T) * g.data.size());
+      write_grid_file<T>(path, g);
+    }
+  });
+}
+
+template <class T>
+int sgrd_read_t(const char* path, int rank, int* dims, void* out, long long cap) {
+  return guarded([&] {
+    std::ifstream is(path, std::ios::binary);
+    std::vector<T> v;
+    if (rank == 1) {
+      v = read_vector<T>(is);
+      dims[0] = static_cast<int>(v.size()); dims[1] = dims[2] = 1;
+    } else if (rank == 2) {
+      Grid2D<T> g = read_grid2d<T>(is);
+      v = g.data; dims[0] = g.width; dims[1] = g.height; dims[2] = 1;
+    } else {
+      Grid3D<T> g = read_grid3d<T>(is);
+      v = g.data; dims[0] = g.nx; dims[1] = g.ny; dims[2] = g.nz;
+    }
+    if (static_cast<long long>(v.size()) <= cap && !v.empty())
+      std::memcpy(out, v.data(), sizeof(T) * v.size());
   });
 }
 
@@ -279,6 +321,24 @@ int ssam_ref_scan(int dtype, const void* in, int len, int lane_count, void* out,
     case F32: return scan_t<float>(in, len, lane_count, out, counters, naive != 0);
     case F64: return scan_t<double>(in, len, lane_count, out, counters, naive != 0);
     case I64: return scan_t<long long>(in, len, lane_count, out, counters, naive != 0);
+  }
+  return 1;
+}
+
+int ssam_ref_sgrd_write(int dtype, const char* path, int rank, const int* dims, const void* data) {
+  switch (dtype) {
+    case F32: return sgrd_write_t<float>(path, rank, dims, data);
+    case F64: return sgrd_write_t<double>(path, rank, dims, data);
+    case I64: return sgrd_write_t<long long>(path, rank, dims, data);
+  }
+  return 1;
+}
+
+int ssam_ref_sgrd_read(int dtype, const char* path, int rank, int* dims, void* out, long long cap) {
+  switch (dtype) {
+    case F32: return sgrd_read_t<float>(path, rank, dims, out, cap);
+    case F64: return sgrd_read_t<double>(path, rank, dims, out, cap);
+    case I64: return sgrd_read_t<long long>(path, rank, dims, out, cap);
   }
   return 1;
 }

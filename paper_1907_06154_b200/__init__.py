@@ -43,7 +43,7 @@ if not os.path.exists(LIB_PATH):
 _lib = C.CDLL(LIB_PATH)
 
 SSAM_OK, SSAM_ERR_INVALID_ARGUMENT, SSAM_ERR_LENGTH, SSAM_ERR_CUDA, SSAM_ERR_NO_DEVICE, \
-    SSAM_ERR_OUT_OF_MEMORY = range(6)
+    SSAM_ERR_OUT_OF_MEMORY, SSAM_ERR_RUNTIME = range(7)
 
 _DT = {np.dtype(np.float32): 0, np.dtype(np.float64): 1, np.dtype(np.int64): 2}
 _NP = {0: np.float32, 1: np.float64, 2: np.int64}
@@ -67,6 +67,10 @@ class NoDevice(RuntimeError):
 
 class OutOfMemory(CudaError):
     pass
+
+
+class GridIOError(RuntimeError):
+    """The reference throws std::runtime_error (grid_io.hpp readers / writers)."""
 
 
 class _Cfg(C.Structure):
@@ -132,6 +136,9 @@ _sig("ssam_b200_counters_conv1d", [_ll, _i, _PC, _PK])
 _sig("ssam_b200_counters_scan", [_ull, _i, _PK])
 _sig("ssam_b200_conv1d_device", [_i, _p, _p, _i, _p, _i, _i, _p])
 _sig("ssam_b200_scan_device", [_i, _p, _p, _sz, _p])
+_sig("ssam_b200_sgrd_info", [C.c_char_p, C.POINTER(_i), C.POINTER(_i), _p])
+_sig("ssam_b200_sgrd_read", [C.c_char_p, _i, _i, _p, _p, _sz, _i, _p])
+_sig("ssam_b200_sgrd_write", [C.c_char_p, _i, _i, _p, _p, _i, _p])
 
 lib = _lib  # raw handle for device-level callers (bench.py, tests)
 
@@ -148,6 +155,7 @@ EXPORTED = [
     "ssam_b200_fill_random", "ssam_b200_max_rel_err", "ssam_b200_conv1d", "ssam_b200_scan",
     "ssam_b200_check_conv1d", "ssam_b200_check_scan", "ssam_b200_counters_conv1d",
     "ssam_b200_counters_scan", "ssam_b200_conv1d_device", "ssam_b200_scan_device",
+    "ssam_b200_sgrd_info", "ssam_b200_sgrd_read", "ssam_b200_sgrd_write",
 ]
 
 
@@ -163,6 +171,8 @@ def _raise(status: int) -> None:
         raise NoDevice(msg)
     if status == SSAM_ERR_OUT_OF_MEMORY:
         raise OutOfMemory(msg)
+    if status == SSAM_ERR_RUNTIME:
+        raise GridIOError(msg)
     raise CudaError(f"status {status}: {msg}")
 
 
@@ -443,6 +453,53 @@ def scan(values, lane_count: int = 32, counters: Optional[OpCounters] = None) ->
     if counters is not None:
         counters._store(cnt)
     return out
+
+
+# -- SGRD grid files (grid_io.hpp:14-158) ---------------------------------------
+
+def sgrd_info(path: str):
+    """(rank, dtype, dims (d0, d1, d2) x-fastest) of an SGRD file."""
+    rank, dt = C.c_int(), C.c_int()
+    dims = np.zeros(3, dtype=np.int32)
+    _raise(_lib.ssam_b200_sgrd_info(os.fsencode(path), C.byref(rank), C.byref(dt),
+                                    dims.ctypes.data))
+    return rank.value, _NP.get(dt.value), tuple(int(d) for d in dims)
+
+
+def _read_sgrd(path: str, dtype, rank: int) -> np.ndarray:
+    _, _, dims = sgrd_info(path)
+    shape = tuple(dims[:rank][::-1])
+    out = np.empty(shape, dtype=dtype)
+    d = np.zeros(3, dtype=np.int32)
+    _raise(_lib.ssam_b200_sgrd_read(os.fsencode(path), _DT[np.dtype(dtype)], rank, d.ctypes.data,
+                                    out.ctypes.data, out.size, 0, None))
+    return out
+
+
+def read_grid2d(path: str, dtype=np.float64) -> np.ndarray:
+    """ssam::read_grid2d<T> (grid_io.hpp:105-111) from a file: an (h, w) array."""
+    return _read_sgrd(path, dtype, 2)
+
+
+def read_grid3d(path: str, dtype=np.float64) -> np.ndarray:
+    """ssam::read_grid3d<T> (grid_io.hpp:113-119): an (nz, ny, nx) array."""
+    return _read_sgrd(path, dtype, 3)
+
+
+def read_vector(path: str, dtype=np.float64) -> np.ndarray:
+    """ssam::read_vector<T> (grid_io.hpp:121-127)."""
+    return _read_sgrd(path, dtype, 1)
+
+
+def write_grid(path: str, grid: np.ndarray) -> None:
+    """ssam::write_grid_file (grid_io.hpp:129-134): rank = grid.ndim (x fastest)."""
+    g = np.asarray(grid)
+    if g.ndim not in (1, 2, 3) or g.dtype not in _DT:
+        raise InvalidArgument("grid io: need a 1-3D float32/float64/int64 array")
+    g = np.ascontiguousarray(g)
+    dims = np.array(list(g.shape[::-1]) + [1] * (3 - g.ndim), dtype=np.int32)
+    _raise(_lib.ssam_b200_sgrd_write(os.fsencode(path), _DT[g.dtype], g.ndim, dims.ctypes.data,
+                                     g.ctypes.data, 0, None))
 
 
 # -- validation / counters without a device ----------------------------------

@@ -573,6 +573,11 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
 
+namespace ssam_b200 {
+// Status + message for the other host-side units (grid_io.cpp).
+int set_error(int status, const std::string& msg) { return fail(status, msg); }
+}  // namespace ssam_b200
+
 // ===========================================================================
 extern "C" {
 

@@ -133,3 +133,31 @@ def scan(d_in, d_out, stream=None) -> None:
     code = _code(d_in)
     _raise(_lib.ssam_b200_scan_device(code, d_in.data_ptr(), d_out.data_ptr(), d_in.numel(),
                                       _s(stream)))
+
+
+def read_grid(path: str, dtype=None, rank: Optional[int] = None, stream=None):
+    """SGRD file -> a new CUDA tensor (payload streamed through pinned buffers)."""
+    import os
+    from . import sgrd_info, _DT
+    torch = _torch()
+    frank, fdt, dims = sgrd_info(path)
+    rank = rank or frank
+    dtype = np.dtype(dtype or fdt)
+    shape = tuple(dims[:rank][::-1])
+    tdt = {0: torch.float32, 1: torch.float64, 2: torch.int64}[_DT[dtype]]
+    t = torch.empty(shape, dtype=tdt, device="cuda")
+    d = np.zeros(3, dtype=np.int32)
+    _raise(_lib.ssam_b200_sgrd_read(os.fsencode(path), _DT[dtype], rank, d.ctypes.data,
+                                    t.data_ptr(), t.numel(), 1, _s(stream)))
+    return t
+
+
+def write_grid(path: str, t, stream=None) -> None:
+    """A contiguous CUDA tensor (1-3D, x fastest) -> SGRD file."""
+    import os
+    code = _code(t)
+    if t.dim() not in (1, 2, 3):
+        raise InvalidArgument("grid io: need a 1-3D tensor")
+    dims = np.array(list(t.shape[::-1]) + [1] * (3 - t.dim()), dtype=np.int32)
+    _raise(_lib.ssam_b200_sgrd_write(os.fsencode(path), code, t.dim(), dims.ctypes.data,
+                                     t.data_ptr(), 1, _s(stream)))
