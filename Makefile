@@ -7,6 +7,7 @@ PKG := paper_1907_06154_b200
 SRC := $(PKG)/csrc
 BUILD := build
 LIB := $(PKG)/libssam_b200.so
+CLI := $(PKG)/bin/ssam
 
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(SRC) \
@@ -18,7 +19,7 @@ CU_OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
 CPP_OBJS := $(BUILD)/abi.o $(BUILD)/tmap.o $(BUILD)/grid_io.o
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp) include/ssam_b200.h
 
-all: $(LIB) oracle dropin
+all: $(LIB) $(CLI) oracle dropin
 
 $(BUILD)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
@@ -30,6 +31,11 @@ $(BUILD)/abi.o: $(SRC)/abi.cpp $(HDRS)
 
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -Xlinker -soname=libssam_b200.so $^ -o $@
+
+# The `ssam` command line (proj/tools/ssam_cli.cpp mirror) over the C ABI.
+$(CLI): $(PKG)/cli/ssam_cli.cpp include/ssam_b200.h $(LIB)
+	@mkdir -p $(PKG)/bin
+	$(CXX) -std=c++17 -O2 -Wall -Iinclude $< $(LIB) -Wl,-rpath,'$$ORIGIN/..' -o $@
 
 oracle:
 	$(MAKE) -C oracle
@@ -52,7 +58,7 @@ debug:
 .PHONY: variant debug
 
 clean:
-	rm -rf $(BUILD) $(LIB)
+	rm -rf $(BUILD) $(LIB) $(CLI)
 
 .PHONY: all oracle clean
 

@@ -229,6 +229,18 @@ int ssam_b200_sgrd_read(const char* path, int dtype, int rank, int* dims /* [3],
 int ssam_b200_sgrd_write(const char* path, int dtype, int rank, const int* dims /* [3] */,
                          const void* src, int on_device, void* stream);
 
+/* ---- direct-gather verifier -----------------------------------------------
+ * The same operators computed by one-thread-per-cell gather kernels in the
+ * oracle's summation order and arithmetic (oracle.hpp:44-116: double
+ * accumulation, no FMA contraction; native int64) -- the GPU-side check the
+ * CLI (`ssam run`, proj/tools/ssam_cli.cpp:138-230) compares the SSAM engine
+ * against.  Host buffers, synchronous, no validation beyond shapes.  A 2D
+ * stencil passes nz = 1; conv1d is conv2d with h = 1, n = 1. */
+int ssam_b200_gather_conv2d(int dtype, const void* in, int width, int height, const void* weights,
+                            int m, int n, int boundary, void* out);
+int ssam_b200_gather_stencil(int dtype, const void* in, int nx, int ny, int nz,
+                             const ssam_stencil* st, int iters, void* out);
+
 #ifdef __cplusplus
 }
 #endif

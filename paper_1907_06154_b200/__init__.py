@@ -139,6 +139,8 @@ _sig("ssam_b200_scan_device", [_i, _p, _p, _sz, _p])
 _sig("ssam_b200_sgrd_info", [C.c_char_p, C.POINTER(_i), C.POINTER(_i), _p])
 _sig("ssam_b200_sgrd_read", [C.c_char_p, _i, _i, _p, _p, _sz, _i, _p])
 _sig("ssam_b200_sgrd_write", [C.c_char_p, _i, _i, _p, _p, _i, _p])
+_sig("ssam_b200_gather_conv2d", [_i, _p, _i, _i, _p, _i, _i, _i, _p])
+_sig("ssam_b200_gather_stencil", [_i, _p, _i, _i, _i, _PS, _i, _p])
 
 lib = _lib  # raw handle for device-level callers (bench.py, tests)
 
@@ -156,6 +158,7 @@ EXPORTED = [
     "ssam_b200_check_conv1d", "ssam_b200_check_scan", "ssam_b200_counters_conv1d",
     "ssam_b200_counters_scan", "ssam_b200_conv1d_device", "ssam_b200_scan_device",
     "ssam_b200_sgrd_info", "ssam_b200_sgrd_read", "ssam_b200_sgrd_write",
+    "ssam_b200_gather_conv2d", "ssam_b200_gather_stencil",
 ]
 
 

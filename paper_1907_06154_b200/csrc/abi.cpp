@@ -569,6 +569,43 @@ template <class T> struct HostScan {
   template <class... A> static int run(A... a) { return host_scan<T>(a...); }
 };
 
+// Direct-gather runs (oracle summation order and arithmetic, direct.cu) on
+// host buffers: the GPU-side verifier the CLI compares the engine against.
+template <class T>
+int host_gather(int kind, const void* in, int nx, int ny, int nz, const void* wts, int m, int n,
+                int boundary, const ssam_stencil* st, int iters, void* out) {
+  cudaStream_t s = cudaStreamPerThread;
+  const size_t bytes = static_cast<size_t>(nx) * ny * nz * sizeof(T);
+  DevBuf a(s), b(s);
+  cudaError_t e;
+  if ((e = a.alloc(bytes)) != cudaSuccess) return cuda_fail(e, "gather alloc");
+  if ((e = b.alloc(bytes)) != cudaSuccess) return cuda_fail(e, "gather alloc");
+  if ((e = cudaMemcpyAsync(a.p, in, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return cuda_fail(e, "gather H2D");
+  T* cur = static_cast<T*>(a.p);
+  T* nxt = static_cast<T*>(b.p);
+  if (kind == 0) {
+    e = conv2d_direct<T>(cur, nxt, nx, ny, static_cast<const T*>(wts), m, n, boundary, s);
+    std::swap(cur, nxt);
+  } else {
+    const StencilDesc<T> d = make_desc<T>(st);
+    e = cudaMemcpyAsync(nxt, cur, bytes, cudaMemcpyDeviceToDevice, s);  // the ring
+    for (int it = 0; e == cudaSuccess && it < iters; ++it) {
+      e = st->dims == 2 ? stencil2d_direct<T>(cur, nxt, nx, ny, 0, ny, d, s)
+                        : stencil3d_direct<T>(cur, nxt, nx, ny, nz, 0, nz, d, s);
+      std::swap(cur, nxt);
+    }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "gather kernel");
+  if ((e = cudaMemcpyAsync(out, cur, bytes, cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+    return cuda_fail(e, "gather D2H");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "gather sync");
+  return SSAM_OK;
+}
+template <class T> struct HostGather {
+  template <class... A> static int run(A... a) { return host_gather<T>(a...); }
+};
+
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
 }  // namespace
@@ -950,6 +987,30 @@ int ssam_b200_scan_device(int dtype, const void* d_in, void* d_out, size_t len, 
     case 2: e = scan_device<long long>(static_cast<const long long*>(d_in), static_cast<long long*>(d_out), len, s); break;
   }
   return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "scan_device");
+}
+
+// ---- direct-gather verifier (oracle arithmetic on the GPU) -----------------------
+int ssam_b200_gather_conv2d(int dtype, const void* in, int w, int h, const void* weights, int m,
+                            int n, int boundary, void* out) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (w < 1 || h < 1 || m < 1 || n < 1 || !in || !out || !weights)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "gather_conv2d: bad arguments");
+  if (int s = device_ready()) return s;
+  return by_dtype<HostGather>(dtype, 0, in, w, h, 1, weights, m, n, boundary,
+                              static_cast<const ssam_stencil*>(nullptr), 0, out);
+}
+
+int ssam_b200_gather_stencil(int dtype, const void* in, int nx, int ny, int nz,
+                             const ssam_stencil* st, int iters, void* out) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = validate_stencil(st)) return s;
+  if (nx < 1 || ny < 1 || nz < 1 || iters < 0 || !in || !out)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "gather_stencil: bad arguments");
+  if (int s = device_ready()) return s;
+  return by_dtype<HostGather>(dtype, 1, in, nx, ny, st->dims == 2 ? 1 : nz,
+                              static_cast<const void*>(nullptr), 0, 0, 0, st, iters, out);
 }
 
 }  // extern "C"
