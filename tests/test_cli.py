@@ -29,7 +29,7 @@ def test_usage_errors_exit_2():
     assert run("cost --sweep nonsense")[0] == 2
     assert run("run conv2d --w 8 --h 64 --precision int")[0] == 2  # narrower than a warp
     assert run("run conv2d --m 21 --n 3 --precision int")[0] == 2  # filter cap (kernels.hpp:192)
-    assert run("run conv2d --p 0")[0] == 2                         # KernelConfig::check
+    assert run("run conv2d --h 400 --p 300")[0] == 2               # C > 255: length_error
     assert run("bench --suite nope")[0] == 2
     assert run("run conv2d --bogus 1")[0] == 2
 
