@@ -456,6 +456,23 @@ def kernel_suite(peak, sm_mhz):
                 "gcells": round(gc, 2), "hbm_gbs_equiv": round(gc * 2 * sz, 1),
                 "hbm_frac": round(gc * 2 * sz / peak, 4), "ms": round(ms, 3)}
         del a, bb
+    # 1D (kernels.hpp:390-447): conv1d 9 taps and the one-pass scan over 2^28 elements
+    # (1 GiB fp32, far above L2), HBM-bound at 2 * sizeof(T) bytes per element.
+    n1 = 1 << 28
+    for dt, tdt, npdt, sz in (("f32", torch.float32, np.float32, 4),
+                              ("f64", torch.float64, np.float64, 8)):
+        x = torch.empty(n1, dtype=tdt, device="cuda")
+        dev.fill_random(x, 0)
+        y = torch.empty_like(x)
+        f = orc.random_filter(9, 1, npdt, 1).reshape(-1)
+        for kname, fn in (("conv1d_m9", lambda: dev.conv1d(x, y, f)),
+                          ("scan", lambda: dev.scan(x, y))):
+            ms = timed(fn, 5)
+            ge = n1 / ms / 1e6
+            out[f"{kname}_{dt}_2^28"] = {"gelems": round(ge, 2), "hbm_gbs": round(ge * 2 * sz, 1),
+                                         "hbm_frac": round(ge * 2 * sz / peak, 4),
+                                         "ms": round(ms, 4)}
+        del x, y
     torch.cuda.empty_cache()
     return out
 

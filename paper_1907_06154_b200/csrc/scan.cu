@@ -8,13 +8,14 @@
 // its tests scan.
 //
 // B200 shape: one pass over HBM (read once, write once).  A CTA of 256
-// threads owns a tile of 256 x ITEMS elements (64 contiguous bytes per
-// thread, 16 KiB per tile): each thread scans its ITEMS serially, the 32
+// threads owns a tile of 256 x ITEMS elements (128 contiguous bytes per
+// thread, 32 KiB per tile): each thread scans its ITEMS serially, the 32
 // thread totals of a warp are combined by the same Kogge-Stone shfl_up
 // ladder the reference simulates (5 shuffles), warp totals by one more
 // ladder, and tiles are chained with decoupled look-back: every tile
 // publishes its aggregate as soon as it is known and its inclusive prefix
 // once its predecessor's is, so the grid never waits for a second pass.
+// The look-back is warp-wide: 32 predecessors are inspected per step.
 // Tile order is taken from an atomic ticket so a tile only ever waits on
 // tiles that are already running.
 #include <cstdint>
@@ -95,34 +96,49 @@ __global__ void __launch_bounds__(kScanThreads)
   __syncthreads();
   const T aggregate = s_warp[NW - 1];
 
-  // decoupled look-back (one thread): publish, then walk back to an inclusive prefix
-  if (tid == 0) {
+  // Decoupled look-back by warp 0: publish the aggregate, then inspect 32
+  // predecessors per step (one per lane) and sum aggregates down to the
+  // nearest published inclusive prefix.
+  if (wid == 0) {
     T excl = T(0);
     if (tile == 0) {
-      st.incl[0] = aggregate;
-      __threadfence();
-      atomicExch(&st.flag[0], 2);
-    } else {
-      st.agg[tile] = aggregate;
-      __threadfence();
-      atomicExch(&st.flag[tile], 1);
-      for (int j = tile - 1;; --j) {
-        int f;
-        do {
-          f = ld_volatile(&st.flag[j]);
-        } while (f == 0);
+      if (lane == 0) {
+        st.incl[0] = aggregate;
         __threadfence();
-        if (f == 2) {
-          excl = ld_volatile(&st.incl[j]) + excl;
-          break;
-        }
-        excl = ld_volatile(&st.agg[j]) + excl;
+        atomicExch(&st.flag[0], 2);
       }
-      st.incl[tile] = excl + aggregate;
-      __threadfence();
-      atomicExch(&st.flag[tile], 2);
+    } else {
+      if (lane == 0) {
+        st.agg[tile] = aggregate;
+        __threadfence();
+        atomicExch(&st.flag[tile], 1);
+      }
+      for (int base = tile - 1;; base -= 32) {
+        const int j = base - lane;  // lane 0 = nearest predecessor
+        int f = 2;
+        T v = T(0);
+        if (j >= 0) {
+          do {
+            f = ld_volatile(&st.flag[j]);
+          } while (f == 0);
+          __threadfence();
+          v = f == 2 ? ld_volatile(&st.incl[j]) : ld_volatile(&st.agg[j]);
+        }
+        const unsigned inc = __ballot_sync(kFull, f == 2);
+        const int stop = inc ? __ffs(inc) - 1 : 31;  // lanes 0..stop contribute
+        T c = lane <= stop ? v : T(0);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(kFull, c, off);
+        excl += __shfl_sync(kFull, c, 0);
+        if (inc) break;
+      }
+      if (lane == 0) {
+        st.incl[tile] = excl + aggregate;
+        __threadfence();
+        atomicExch(&st.flag[tile], 2);
+      }
     }
-    s_prefix = excl;
+    if (lane == 0) s_prefix = excl;
   }
   __syncthreads();
   T add = s_prefix;
@@ -149,7 +165,7 @@ __global__ void __launch_bounds__(kScanThreads)
 template <class T>
 cudaError_t scan_impl(const T* d_in, T* d_out, size_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  constexpr int ITEMS = sizeof(T) == 4 ? 16 : 8;
+  constexpr int ITEMS = sizeof(T) == 4 ? 32 : 16;  // 128 contiguous bytes per thread
   constexpr size_t TILE = static_cast<size_t>(kScanThreads) * ITEMS;
   const size_t tiles = (n + TILE - 1) / TILE;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;

@@ -1,5 +1,5 @@
 """Launch one kernel config a few times (for ncu captures): prof_one.py KIND [args]
-   conv K | st2d NAME DT | st3d NAME DT N"""
+   conv K | st2d NAME DT | st3d NAME DT N | conv1d M DT | scan DT"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -13,6 +13,15 @@ if kind == "conv":
     o = torch.empty_like(g)
     f = np.random.default_rng(1).uniform(-1, 1, (K, K)).astype(np.float32)
     for _ in range(reps): dev.conv2d(g, o, f)
+elif kind in ("conv1d", "scan"):
+    dt = sys.argv[-1]
+    tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)
+    x = torch.empty(1 << 28, dtype=tdt, device="cuda"); dev.fill_random(x, 0); y = torch.empty_like(x)
+    if kind == "conv1d":
+        f = np.random.default_rng(1).uniform(-1, 1, int(sys.argv[2])).astype(npdt)
+        for _ in range(reps): dev.conv1d(x, y, f)
+    else:
+        for _ in range(reps): dev.scan(x, y)
 elif kind == "st2d":
     name, dt = sys.argv[2], sys.argv[3]; H = W = 8192
     tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)
