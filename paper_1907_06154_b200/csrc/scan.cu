@@ -7,17 +7,21 @@
 // (oracle::scan_naive, oracle.hpp:118-127) -- exact for int64, the only type
 // its tests scan.
 //
-// B200 shape: one pass over HBM (read once, write once).  A CTA of 256
-// threads owns a tile of 256 x ITEMS elements (128 contiguous bytes per
-// thread, 32 KiB per tile): each thread scans its ITEMS serially, the 32
-// thread totals of a warp are combined by the same Kogge-Stone shfl_up
-// ladder the reference simulates (5 shuffles), warp totals by one more
-// ladder, and tiles are chained with decoupled look-back: every tile
-// publishes its aggregate as soon as it is known and its inclusive prefix
-// once its predecessor's is, so the grid never waits for a second pass.
-// The look-back is warp-wide: 32 predecessors are inspected per step.
-// Tile order is taken from an atomic ticket so a tile only ever waits on
-// tiles that are already running.
+// B200 shape: reduce-then-scan over 256 x 8 rows x 16-byte tiles.
+//   1. scan_reduce_kernel: one CTA per tile sums it (read n).
+//   2. scan_carry_kernel: one CTA turns the tile sums into exclusive tile
+//      prefixes (tiles / 1024 block scans; 32 K tiles for 2^28 fp32).
+//   3. scan_tile_kernel: one CTA per tile scans it from its prefix (read n,
+//      write n).
+// Within a tile every warp owns rows of 32 x 16 bytes (coalesced 512-byte
+// loads and stores); per row each lane scans its 16 bytes serially and the
+// 32 lane totals run the same Kogge-Stone shfl_up ladder the reference
+// simulates (5 shuffles), warp totals one more ladder.  A single-pass
+// decoupled look-back (measured here at 2.0-2.5 TB/s on B200: the
+// inclusive-prefix chain across ~600 co-resident tiles, not HBM, bound it)
+// would also make floating-point results depend on timing; this order is
+// fixed, so every run is bit-identical.  Traffic is 3 x n element moves
+// against the 2 x n minimum.
 #include <cstdint>
 
 #include "common.cuh"
@@ -28,166 +32,169 @@ namespace ssam_b200 {
 namespace {
 
 constexpr int kScanThreads = 256;
+constexpr int kCarryThreads = 1024;
 
 template <class T>
-struct ScanState {
-  int* ticket;      // next tile to hand out
-  int* flag;        // per tile: 0 nothing, 1 aggregate, 2 inclusive prefix
-  T* agg;
-  T* incl;
+struct ScanTile {
+  static constexpr int VQ = 16 / sizeof(T);
+  static constexpr int ROWS = 8;  // 16 KiB (fp32) / 32 KiB (64-bit) tiles
+  static constexpr int TILE = kScanThreads * ROWS * VQ;
 };
 
+// Loads warp `wid`'s rows of tile `tile` (zeros past n); returns whether the
+// tile is whole and 16-byte aligned (vector path).
 template <class T>
-__device__ __forceinline__ T ld_volatile(const T* p) {
-  return *reinterpret_cast<const volatile T*>(p);
+__device__ __forceinline__ bool load_rows(const T* __restrict__ in, size_t n, int tile, int wid,
+                                          int lane, T (&v)[ScanTile<T>::ROWS][ScanTile<T>::VQ],
+                                          size_t& wbase) {
+  constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS, TILE = ScanTile<T>::TILE;
+  wbase = static_cast<size_t>(tile) * TILE + static_cast<size_t>(wid) * ROWS * 32 * VQ;
+  const bool full = static_cast<size_t>(tile + 1) * TILE <= n &&
+                    (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r) {
+    const size_t at = wbase + static_cast<size_t>(r) * 32 * VQ + lane * VQ;
+    if (full) {
+      ldg_q<T, VQ>(in + at, v[r]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < VQ; ++q) v[r][q] = at + q < n ? in[at + q] : T(0);
+    }
+  }
+  return full;
 }
 
-template <class T, int ITEMS>
+template <class T>
 __global__ void __launch_bounds__(kScanThreads)
-    scan_kernel(const T* __restrict__ in, T* __restrict__ out, size_t n, ScanState<T> st) {
-  constexpr int TILE = kScanThreads * ITEMS;
-  constexpr int NW = kScanThreads / 32;
-  __shared__ int s_tile;
+    scan_reduce_kernel(const T* __restrict__ in, size_t n, T* __restrict__ tile_sum) {
+  constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS;
+  __shared__ T s_warp[kScanThreads / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T v[ROWS][VQ];
+  size_t wbase;
+  load_rows<T>(in, n, blockIdx.x, wid, lane, v, wbase);
+  T x = T(0);
+#pragma unroll
+  for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+    for (int q = 0; q < VQ; ++q) x += v[r][q];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(kFull, x, off);
+  if (lane == 0) s_warp[wid] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    T t = T(0);
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) t += s_warp[w];
+    tile_sum[blockIdx.x] = t;
+  }
+}
+
+// Exclusive prefix of the tile sums, 1024 at a time with a running carry.
+template <class T>
+__global__ void __launch_bounds__(kCarryThreads)
+    scan_carry_kernel(const T* __restrict__ tile_sum, T* __restrict__ tile_prefix, int tiles) {
+  __shared__ T s_warp[kCarryThreads / 32];
+  __shared__ T s_carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_carry = T(0);
+  __syncthreads();
+  for (int base = 0; base < tiles; base += kCarryThreads) {
+    const int i = base + threadIdx.x;
+    const T x = i < tiles ? tile_sum[i] : T(0);
+    T t = x;
+#pragma unroll
+    for (int d = 1; d < 32; d *= 2) {
+      const T u = __shfl_up_sync(kFull, t, d);
+      if (lane >= d) t += u;
+    }
+    if (lane == 31) s_warp[wid] = t;
+    __syncthreads();
+    if (wid == 0) {
+      T w = s_warp[lane];
+#pragma unroll
+      for (int d = 1; d < 32; d *= 2) {
+        const T u = __shfl_up_sync(kFull, w, d);
+        if (lane >= d) w += u;
+      }
+      s_warp[lane] = w;
+    }
+    __syncthreads();
+    const T carry = s_carry;
+    T ex = __shfl_up_sync(kFull, t, 1);
+    if (lane == 0) ex = T(0);
+    const T pre = carry + ((wid > 0 ? s_warp[wid - 1] : T(0)) + ex);
+    if (i < tiles) tile_prefix[i] = pre;
+    __syncthreads();
+    if (threadIdx.x == kCarryThreads - 1) s_carry = pre + x;
+    __syncthreads();
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kScanThreads)
+    scan_tile_kernel(const T* __restrict__ in, T* __restrict__ out, size_t n,
+                     const T* __restrict__ tile_prefix) {
+  constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS, NW = kScanThreads / 32;
   __shared__ T s_warp[NW];
-  __shared__ T s_prefix;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(st.ticket, 1);
-  __syncthreads();
-  const int tile = s_tile;
-  const size_t base = static_cast<size_t>(tile) * TILE + static_cast<size_t>(tid) * ITEMS;
-
-  // thread-serial inclusive scan of ITEMS contiguous elements
-  T v[ITEMS];
-  constexpr int VQ = 16 / sizeof(T);
-  const bool full = base + ITEMS <= n && (reinterpret_cast<uintptr_t>(in + base) & 15) == 0;
-  if (full) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  T v[ROWS][VQ];
+  size_t wbase;
+  const bool full = load_rows<T>(in, n, blockIdx.x, wid, lane, v, wbase) &&
+                    (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  T carry = T(0);  // running total of the warp's earlier rows
 #pragma unroll
-    for (int c = 0; c < ITEMS / VQ; ++c) {
-      T tmp[VQ];
-      ldg_q<T, VQ>(in + base + c * VQ, tmp);
+  for (int r = 0; r < ROWS; ++r) {
 #pragma unroll
-      for (int q = 0; q < VQ; ++q) v[c * VQ + q] = tmp[q];
+    for (int q = 1; q < VQ; ++q) v[r][q] += v[r][q - 1];
+    T t = v[r][VQ - 1];
+#pragma unroll
+    for (int d = 1; d < 32; d *= 2) {
+      const T u = __shfl_up_sync(kFull, t, d);
+      if (lane >= d) t += u;
     }
-  } else {
+    T ex = __shfl_up_sync(kFull, t, 1);  // exclusive lane prefix within the row
+    if (lane == 0) ex = T(0);
+    ex += carry;
 #pragma unroll
-    for (int i = 0; i < ITEMS; ++i) v[i] = base + i < n ? in[base + i] : T(0);
+    for (int q = 0; q < VQ; ++q) v[r][q] += ex;
+    carry += __shfl_sync(kFull, t, 31);
   }
-#pragma unroll
-  for (int i = 1; i < ITEMS; ++i) v[i] += v[i - 1];
-
-  // Kogge-Stone over the warp's thread totals (shift 1, 2, 4, 8, 16)
-  T t = v[ITEMS - 1];
-#pragma unroll
-  for (int d = 1; d < 32; d *= 2) {
-    const T u = __shfl_up_sync(kFull, t, d);
-    if (lane >= d) t += u;
-  }
-  if (lane == 31) s_warp[wid] = t;
+  if (lane == 0) s_warp[wid] = carry;
   __syncthreads();
-  if (wid == 0) {
-    T w = lane < NW ? s_warp[lane] : T(0);
+  T add = tile_prefix[blockIdx.x];
+  for (int w = 0; w < wid; ++w) add += s_warp[w];
 #pragma unroll
-    for (int d = 1; d < NW; d *= 2) {
-      const T u = __shfl_up_sync(kFull, w, d);
-      if (lane >= d) w += u;
-    }
-    if (lane < NW) s_warp[lane] = w;  // inclusive warp prefixes
-  }
-  __syncthreads();
-  const T aggregate = s_warp[NW - 1];
-
-  // Decoupled look-back by warp 0: publish the aggregate, then inspect 32
-  // predecessors per step (one per lane) and sum aggregates down to the
-  // nearest published inclusive prefix.
-  if (wid == 0) {
-    T excl = T(0);
-    if (tile == 0) {
-      if (lane == 0) {
-        st.incl[0] = aggregate;
-        __threadfence();
-        atomicExch(&st.flag[0], 2);
-      }
+  for (int r = 0; r < ROWS; ++r) {
+    const size_t at = wbase + static_cast<size_t>(r) * 32 * VQ + lane * VQ;
+#pragma unroll
+    for (int q = 0; q < VQ; ++q) v[r][q] += add;
+    if (full) {
+      st_q<T, VQ>(out + at, v[r]);
     } else {
-      if (lane == 0) {
-        st.agg[tile] = aggregate;
-        __threadfence();
-        atomicExch(&st.flag[tile], 1);
-      }
-      for (int base = tile - 1;; base -= 32) {
-        const int j = base - lane;  // lane 0 = nearest predecessor
-        int f = 2;
-        T v = T(0);
-        if (j >= 0) {
-          do {
-            f = ld_volatile(&st.flag[j]);
-          } while (f == 0);
-          __threadfence();
-          v = f == 2 ? ld_volatile(&st.incl[j]) : ld_volatile(&st.agg[j]);
-        }
-        const unsigned inc = __ballot_sync(kFull, f == 2);
-        const int stop = inc ? __ffs(inc) - 1 : 31;  // lanes 0..stop contribute
-        T c = lane <= stop ? v : T(0);
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) c += __shfl_down_sync(kFull, c, off);
-        excl += __shfl_sync(kFull, c, 0);
-        if (inc) break;
-      }
-      if (lane == 0) {
-        st.incl[tile] = excl + aggregate;
-        __threadfence();
-        atomicExch(&st.flag[tile], 2);
-      }
+      for (int q = 0; q < VQ; ++q)
+        if (at + q < n) out[at + q] = v[r][q];
     }
-    if (lane == 0) s_prefix = excl;
-  }
-  __syncthreads();
-  T add = s_prefix;
-  if (wid > 0) add += s_warp[wid - 1];
-  const T tprev = __shfl_up_sync(kFull, t, 1);
-  if (lane > 0) add += tprev;
-#pragma unroll
-  for (int i = 0; i < ITEMS; ++i) v[i] += add;
-  if (full) {
-#pragma unroll
-    for (int c = 0; c < ITEMS / VQ; ++c) {
-      T tmp[VQ];
-#pragma unroll
-      for (int q = 0; q < VQ; ++q) tmp[q] = v[c * VQ + q];
-      st_q<T, VQ>(out + base + c * VQ, tmp);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i)
-      if (base + i < n) out[base + i] = v[i];
   }
 }
 
 template <class T>
 cudaError_t scan_impl(const T* d_in, T* d_out, size_t n, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  constexpr int ITEMS = sizeof(T) == 4 ? 32 : 16;  // 128 contiguous bytes per thread
-  constexpr size_t TILE = static_cast<size_t>(kScanThreads) * ITEMS;
+  constexpr size_t TILE = ScanTile<T>::TILE;
   const size_t tiles = (n + TILE - 1) / TILE;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-  // scratch: ticket + flags, then the two value arrays (stream-ordered pool)
-  const size_t fbytes = (tiles + 1) * sizeof(int);
-  const size_t voff = (fbytes + 15) / 16 * 16;
-  const size_t bytes = voff + 2 * tiles * sizeof(T);
-  void* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&scratch, bytes, s);
+  T* scratch = nullptr;  // tile sums, then tile prefixes (stream-ordered pool)
+  cudaError_t e = cudaMallocAsync(&scratch, 2 * tiles * sizeof(T), s);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(scratch, 0, fbytes, s);
-  if (e == cudaSuccess) {
-    ScanState<T> st;
-    st.ticket = static_cast<int*>(scratch);
-    st.flag = st.ticket + 1;
-    st.agg = reinterpret_cast<T*>(static_cast<char*>(scratch) + voff);
-    st.incl = st.agg + tiles;
-    scan_kernel<T, ITEMS><<<static_cast<unsigned>(tiles), kScanThreads, 0, s>>>(d_in, d_out, n,
-                                                                                st);
-    note_launch();
-    e = cudaGetLastError();
-  }
+  const unsigned g = static_cast<unsigned>(tiles);
+  scan_reduce_kernel<T><<<g, kScanThreads, 0, s>>>(d_in, n, scratch);
+  scan_carry_kernel<T><<<1, kCarryThreads, 0, s>>>(scratch, scratch + tiles,
+                                                    static_cast<int>(tiles));
+  scan_tile_kernel<T><<<g, kScanThreads, 0, s>>>(d_in, d_out, n, scratch + tiles);
+  for (int k = 0; k < 3; ++k) note_launch();
+  e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
   return e;
 }
