@@ -42,7 +42,7 @@ inline int conv_fma_min_k() {
   return v;
 }
 
-template <class T, int Q, int NR, int MC, int RY, bool EXACT, int CAP>
+template <class T, int Q, int NR, int MC, int RY, bool EXACT, int CAP, class Mask = DenseMask>
 cudaError_t launch_fma2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int RB = RY > 4 ? RY : 4;
   constexpr int D = 3;
@@ -73,7 +73,7 @@ cudaError_t launch_fma2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   p.ring = a.ring;
   p.vec_ok = 1;
   std::memcpy(p.coef, a.coef, sizeof(T) * a.M * NR);
-  auto kern = ssam2d_fma_kernel<T, Q, NR, MC, RY, RB, D, EXACT, CAP>;
+  auto kern = ssam2d_fma_kernel<T, Q, NR, MC, Mask, RY, RB, D, EXACT, CAP>;
   const size_t smem = fma2d_smem<T, Q, NR, RB, D, EXACT>(kWarpsPerBlock, a.M);
   const int gx = (p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const dim3 grid(gx, (rows + p.seg - 1) / p.seg);

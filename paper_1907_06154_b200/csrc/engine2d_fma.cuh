@@ -25,9 +25,13 @@
 //    constant-bank operands; run-time widths (MC = 0) loop over columns with
 //    each column's NR weights broadcast from shared memory.
 //
+// Stencils use it too (compile-time tap masks, interior-only stores): the
+// tall star footprints (2ds25pt) otherwise spend a quarter of their issue
+// slots on the light kernel's one-row window shifts.
+//
 // Arithmetic per output is that of the light kernel's compile-time path
-// (engine2d.cuh ssam_row_ct): colpart_j is the serial FMA chain over
-// t = 0..NR-1 starting with a multiply; acc = colpart_0, then
+// (engine2d.cuh ssam_row_ct): colpart_j is the serial FMA chain over the
+// column's taps in t order starting with a multiply; acc = colpart_0, then
 // acc = shift_up(acc) + colpart_j; accr likewise from the right; then
 // acc += shift_down(accr).  Results are bit-identical to that kernel.
 //
@@ -61,7 +65,7 @@ __host__ __device__ constexpr size_t fma2d_smem(int warps, int m) {
          static_cast<size_t>(m) * ((NR * sizeof(T) + 15) / 16 * 16);
 }
 
-template <class T, int Q, int NR, int MC, int RY, int RB, int D, bool EXACT, int CAP>
+template <class T, int Q, int NR, int MC, class Mask, int RY, int RB, int D, bool EXACT, int CAP>
 __global__ void __launch_bounds__(128)
     ssam2d_fma_kernel(const __grid_constant__ Ssam2DTmaParams<T, CAP> P) {
   static_assert(RB % RY == 0, "passes never straddle boxes");
@@ -110,7 +114,9 @@ __global__ void __launch_bounds__(128)
   const int dmis = xl - base;  // EXACT: misalignment of the lanes in the box (warp-uniform)
   const int x0 = xl + Q * lane;
   // columns of this lane that are outputs of this warp and of the image
-  const int xlo = max(x_out0, 0), xhi = min(x_out0 + p.V, p.W);
+  // (stencils: only the interior [ring, W-ring) is written; rows are clamped by the caller)
+  const int xlo = max(x_out0, p.bmode == kBndStencil ? p.ring : 0);
+  const int xhi = min(x_out0 + p.V, p.bmode == kBndStencil ? p.W - p.ring : p.W);
   uint32_t qmask = 0;
 #pragma unroll
   for (int q = 0; q < Q; ++q) qmask |= (x0 + q >= xlo && x0 + q < xhi) ? 1u << q : 0u;
@@ -168,13 +174,24 @@ __global__ void __launch_bounds__(128)
       }
     }
   };
-  // Column partial of filter column j (weights c) for output row r.
-  auto colpart = [&](const T (&win)[NW][Q], const T (&c)[NRP], int r, T (&cp)[Q]) {
+  // Column partial of filter column j (weights c) for output row r: the
+  // serial FMA chain over the column's taps (Mask), first tap a multiply.
+  auto colpart = [&](const T (&win)[NW][Q], const T (&c)[NRP], int j, int r, T (&cp)[Q]) {
+    bool any = false;
 #pragma unroll
-    for (int t = 0; t < NR; ++t)
+    for (int t = 0; t < NR; ++t) {
+      if (Mask::has(j, t)) {
 #pragma unroll
-      for (int q = 0; q < Q; ++q)
-        cp[q] = t == 0 ? c[t] * win[r + t][q] : fma_t(c[t], win[r + t][q], cp[q]);
+        for (int q = 0; q < Q; ++q)
+          cp[q] = any ? fma_t(c[t], win[r + t][q], cp[q]) : c[t] * win[r + t][q];
+        any = true;
+      }
+    }
+    if (!any) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) cp[q] = T(0);
+    }
+    return any;
   };
 
   // Prologue: stream rows OFF .. OFF+NR-2 into window rows 0 .. NR-2.
@@ -207,7 +224,7 @@ __global__ void __launch_bounds__(128)
       T c[NRP];
       load_col(0, c);
 #pragma unroll
-      for (int r = 0; r < RY; ++r) colpart(win, c, r, acc[r]);
+      for (int r = 0; r < RY; ++r) colpart(win, c, 0, r, acc[r]);
     }
 #pragma unroll(UNROLL ? 20 : 1)
     for (int j = 1; j <= L; ++j) {
@@ -216,10 +233,12 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
       for (int r = 0; r < RY; ++r) {
         T cp[Q];
-        colpart(win, c, r, cp);
+        const bool any = colpart(win, c, j, r, cp);
         shift_up1<T, Q>(acc[r]);
+        if (any) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q) acc[r][q] += cp[q];
+          for (int q = 0; q < Q; ++q) acc[r][q] += cp[q];
+        }
       }
     }
     if (R > 0) {
@@ -228,7 +247,7 @@ __global__ void __launch_bounds__(128)
         T c[NRP];
         load_col(M - 1, c);
 #pragma unroll
-        for (int r = 0; r < RY; ++r) colpart(win, c, r, accr[r]);
+        for (int r = 0; r < RY; ++r) colpart(win, c, M - 1, r, accr[r]);
       }
       // right chain: columns M-2..L+1 flow down (shfl_down)
 #pragma unroll(UNROLL ? 20 : 1)
@@ -238,10 +257,12 @@ __global__ void __launch_bounds__(128)
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
           T cp[Q];
-          colpart(win, c, r, cp);
+          const bool any = colpart(win, c, j, r, cp);
           shift_down1<T, Q>(accr[r]);
+          if (any) {
 #pragma unroll
-          for (int q = 0; q < Q; ++q) accr[r][q] += cp[q];
+            for (int q = 0; q < Q; ++q) accr[r][q] += cp[q];
+          }
         }
       }
 #pragma unroll

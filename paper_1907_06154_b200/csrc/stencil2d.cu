@@ -29,10 +29,25 @@ constexpr int st_q(int k) {
   return sizeof(T) == 4 ? (k <= 3 ? 8 : 4) : (std::is_same<T, double>::value && k <= 3 ? 4 : 2);
 }
 
+// Tall footprints (order >= 4: 9+ rows) take the FMA engine's RY-row
+// passes (engine2d_fma.cuh) when the rows are TMA-eligible; SSAM_B200_ST2D_FMA=0
+// keeps them on the light kernel.
+inline bool st2d_fma_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SSAM_B200_ST2D_FMA");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 template <class T, int Q, int K, class Mask>
 cudaError_t st2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
   constexpr int QQ = st_q<T>(K);
+  if constexpr (K >= 4 && !std::is_same<T, long long>::value) {
+    if (st2d_fma_enabled() && fma_eligible(a))
+      return launch_fma2d<T, QQ, M, M, 4, false, M * M, Mask>(a, s);
+  }
   return launch_ssam2d<T, QQ, M, M, Mask, pf_rows(M), M * M>(a, s);
 }
 
