@@ -173,6 +173,13 @@ int ssam_b200_stencil2d_tb_max(int dtype, const ssam_stencil* st);
 int ssam_b200_stencil3d_sweep(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
                               int z_begin, int z_end, const ssam_stencil* st, void* stream);
 
+/* tb fused 3D sweeps (temporal blocking, tb = 2 for order-1 stencils) over
+ * the whole grid; SSAM_ERR_INVALID_ARGUMENT if no fused kernel exists.
+ * d_out's ring must equal d_in's.  _tb_max: deepest fused block (1 = none). */
+int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
+                           const ssam_stencil* st, int tb, void* stream);
+int ssam_b200_stencil3d_tb_max(int dtype, const ssam_stencil* st);
+
 /* iters sweeps with ping-pong buffers.  d_a holds the input; d_b is scratch
  * of the same size whose ring this call initialises.  *d_result receives
  * d_a or d_b, whichever holds the final generation.  tb: temporal block
@@ -182,6 +189,8 @@ int ssam_b200_stencil2d_run(int dtype, void* d_a, void* d_b, int width, int heig
                             void** d_result);
 int ssam_b200_stencil3d_run(int dtype, void* d_a, void* d_b, int nx, int ny, int nz,
                             const ssam_stencil* st, int iters, void* stream, void** d_result);
+/* (stencil3d_run fuses sweeps in pairs with ssam_b200_stencil3d_tb where
+ * available: same results, half the HBM passes.) */
 
 /* Device SplitMix64 fill, bit-identical to the reference's random_grid2d/3d:
  * element i receives stream draw (first + i) of seed (rng.hpp, grid.hpp:52-66). */

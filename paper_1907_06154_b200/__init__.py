@@ -122,6 +122,8 @@ _sig("ssam_b200_stencil2d_sweep", [_i, _p, _p, _i, _i, _i, _i, _PS, _p])
 _sig("ssam_b200_stencil2d_tb", [_i, _p, _p, _i, _i, _PS, _i, _p])
 _sig("ssam_b200_stencil2d_tb_max", [_i, _PS])
 _sig("ssam_b200_stencil3d_sweep", [_i, _p, _p, _i, _i, _i, _i, _i, _PS, _p])
+_sig("ssam_b200_stencil3d_tb", [_i, _p, _p, _i, _i, _i, _PS, _i, _p])
+_sig("ssam_b200_stencil3d_tb_max", [_i, _PS])
 _sig("ssam_b200_stencil2d_run", [_i, _p, _p, _i, _i, _PS, _i, _i, _p, C.POINTER(_p)])
 _sig("ssam_b200_stencil3d_run", [_i, _p, _p, _i, _i, _i, _PS, _i, _p, C.POINTER(_p)])
 _sig("ssam_b200_fill_random", [_i, _p, _sz, _u64, _u64, _p])
@@ -158,7 +160,8 @@ EXPORTED = [
     "ssam_b200_check_conv1d", "ssam_b200_check_scan", "ssam_b200_counters_conv1d",
     "ssam_b200_counters_scan", "ssam_b200_conv1d_device", "ssam_b200_scan_device",
     "ssam_b200_sgrd_info", "ssam_b200_sgrd_read", "ssam_b200_sgrd_write",
-    "ssam_b200_gather_conv2d", "ssam_b200_gather_stencil",
+    "ssam_b200_gather_conv2d", "ssam_b200_gather_stencil", "ssam_b200_stencil3d_tb",
+    "ssam_b200_stencil3d_tb_max",
 ]
 
 

@@ -393,10 +393,29 @@ cudaError_t run3d(T* a, T* b, int nx, int ny, int nz, const StencilDesc<T>& d, i
   if (e != cudaSuccess) return e;
   T* cur = a;
   T* nxt = b;
-  for (int it = 0; it < iters; ++it) {
-    e = stencil3d_sweep<T>(cur, nxt, nx, ny, nz, 0, nz, d, s);
-    if (e != cudaSuccess) return e;
+  const int dtype = sizeof(T) == 4 ? 0 : (std::is_same<T, double>::value ? 1 : 2);
+  const int tb = (d.order == 1 && classify3d(d.taps, 1) == Shape3D::star)
+                     ? stencil3d_tb_max(dtype, d.order)
+                     : 1;
+  int done = 0;
+  while (done < iters) {
+    int depth = 1;
+    if (tb > 1 && iters - done >= tb) {
+      depth = tb;
+      e = stencil3d_tb<T>(cur, nxt, nx, ny, nz, d, tb, s);
+      if (e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        depth = 1;
+      } else if (e != cudaSuccess) {
+        return e;
+      }
+    }
+    if (depth == 1) {
+      e = stencil3d_sweep<T>(cur, nxt, nx, ny, nz, 0, nz, d, s);
+      if (e != cudaSuccess) return e;
+    }
     std::swap(cur, nxt);
+    done += depth;
   }
   *result = cur;
   return cudaSuccess;
@@ -1011,6 +1030,32 @@ int ssam_b200_gather_stencil(int dtype, const void* in, int nx, int ny, int nz,
   if (int s = device_ready()) return s;
   return by_dtype<HostGather>(dtype, 1, in, nx, ny, st->dims == 2 ? 1 : nz,
                               static_cast<const void*>(nullptr), 0, 0, 0, st, iters, out);
+}
+
+int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
+                           const ssam_stencil* st, int tb, void* stream) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = validate_stencil(st)) return s;
+  if (st->dims != 3) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d: needs a 3D stencil");
+  if (int s = device_ready()) return s;
+  cudaError_t e = cudaErrorNotSupported;
+  const cudaStream_t s = as_stream(stream);
+  switch (dtype) {
+    case 0: e = stencil3d_tb<float>(static_cast<const float*>(d_in), static_cast<float*>(d_out), nx, ny, nz, make_desc<float>(st), tb, s); break;
+    case 1: e = stencil3d_tb<double>(static_cast<const double*>(d_in), static_cast<double*>(d_out), nx, ny, nz, make_desc<double>(st), tb, s); break;
+    default: break;
+  }
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d_tb: no fused kernel for this case");
+  }
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "stencil3d_tb");
+}
+
+int ssam_b200_stencil3d_tb_max(int dtype, const ssam_stencil* st) {
+  if (!st || st->dims != 3 || !dtype_ok(dtype)) return 1;
+  return stencil3d_tb_max(dtype, st->order);
 }
 
 }  // extern "C"

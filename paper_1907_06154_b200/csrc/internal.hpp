@@ -59,6 +59,13 @@ template <class T>
 cudaError_t stencil3d_sweep(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin,
                             int z_end, const StencilDesc<T>& st, cudaStream_t s);
 
+// Tb fused 3D sweeps (temporal blocking) over the whole grid.  Returns
+// cudaErrorNotSupported when no fused kernel exists (the caller then sweeps).
+template <class T>
+cudaError_t stencil3d_tb(const T* d_in, T* d_out, int nx, int ny, int nz,
+                         const StencilDesc<T>& st, int tb, cudaStream_t s);
+int stencil3d_tb_max(int dtype, int order);
+
 // ---- direct-gather kernels (generic path: any order / tap set) -------------
 // Bit-faithful to the oracle's summation order (double accumulation for FP,
 // no FMA contraction), used where no SSAM specialisation applies.

@@ -96,6 +96,20 @@ def stencil3d_sweep(d_in, d_out, st: Stencil, z_begin: int = 0, z_end: Optional[
                                           _s(stream)))
 
 
+def stencil3d_tb(d_in, d_out, st: Stencil, tb: int, stream=None) -> None:
+    """tb fused 3D sweeps (order-1 stencils, tb = 2); d_out's ring must equal d_in's."""
+    code = _code(d_in)
+    nz, ny, nx = d_in.shape
+    sa = _StencilArgs(st, _np_dtype(code))
+    _raise(_lib.ssam_b200_stencil3d_tb(code, d_in.data_ptr(), d_out.data_ptr(), nx, ny, nz,
+                                       sa.ref, tb, _s(stream)))
+
+
+def stencil3d_tb_max(st: Stencil, dtype) -> int:
+    sa = _StencilArgs(st, dtype)
+    return int(_lib.ssam_b200_stencil3d_tb_max(_DT[np.dtype(dtype)], sa.ref))
+
+
 def stencil3d_run(d_a, d_b, st: Stencil, iters: int, stream=None):
     code = _code(d_a)
     nz, ny, nx = d_a.shape
