@@ -191,7 +191,8 @@ def run_reference_arm(args, rank: int, world: int):
 def workload_config(world: int, args):
     return {"workload": f"{STENCIL} f32 {NX}x{NY}x({NZ_PER_GPU}*N) z-slab, NVLink halo exchange",
             "stencil": STENCIL, "nx": NX, "ny": NY, "nz": NZ_PER_GPU * world,
-            "nz_per_gpu": NZ_PER_GPU, "iters_per_step": args.iters, "temporal_block": 1,
+            "nz_per_gpu": NZ_PER_GPU, "iters_per_step": args.iters,
+            "temporal_block": max(1, args.tb),
             "parallelism": f"z-slab x{world}", "seed": 0,
             "l2": "no flush needed: 8 GiB per buffer >> 126 MB L2"}
 
@@ -212,7 +213,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     peak, peak_kind, sm_max_nominal = load_peaks()
     st = ssam.convert_stencil(ssam.make_benchmark_stencil(STENCIL), np.float32)
     k = st.order
-    slab = decompose(NZ_PER_GPU * world, world, rank, k)
+    tb = max(1, args.tb)
+    slab = decompose(NZ_PER_GPU * world, world, rank, k, ghost=k * tb)
     a = torch.empty((slab.nz_local, NY, NX), dtype=torch.float32, device="cuda")
     fill_slab(a, slab, NX, NY, seed=0)
     b = a.clone()
@@ -233,7 +235,21 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         else:
             dev.stencil3d_sweep(cur, nxt, st, zb, ze)
 
-    runner = SlabRunner(slab, sweep, comm_stream=comm)
+    rlo, rhi = slab.ring_bounds()
+
+    def fused(cur, nxt, zb, ze):
+        if ze <= zb:
+            return
+        if timing["on"] and zb == slab.compute_range()[0] and world == 1:
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            dev.stencil3d_tb(cur, nxt, st, tb, zb, ze, rlo, rhi)
+            e.record()
+            launch_ms.append((s, e))
+        else:
+            dev.stencil3d_tb(cur, nxt, st, tb, zb, ze, rlo, rhi)
+
+    runner = SlabRunner(slab, sweep, comm_stream=comm, fused=fused if tb > 1 else None, tb=tb)
 
     def barrier():
         if world > 1:
@@ -280,9 +296,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         durs = [s.elapsed_time(e) for s, e in launch_ms]
         mean_ms = sum(durs) / len(durs)
     else:
-        mean_ms = max_ms / (args.steps * args.iters)
+        mean_ms = max_ms / (args.steps * args.iters / tb)
+    # a fused launch reads and writes every cell once for its tb updates
     achieved = 8.0 * cells_per_launch / (mean_ms / 1e3) / 1e9
-    traffic = load_traffic().get(f"ssam3d_{STENCIL}_f32_{NX}x{NY}x{slab.nz_local}")
+    traffic = load_traffic().get(f"ssam3d_{STENCIL}_f32_{NX}x{NY}x{slab.nz_local}"
+                                 + ("_tb2" if tb > 1 else ""))
 
     # free the slab before the e2e / per-kernel phases
     del a, b
@@ -313,11 +331,13 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference SplitMix64 stream, seed 0, generated on device)",
             "config": workload_config(world, args),
-            "hbm_gbs_algorithmic": round(value * 8.0, 1),
+            "hbm_gbs_algorithmic": round(value * 8.0 / tb, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": f"ssam3d_halo_kernel {STENCIL} f32",
+                         "kernel": (f"ssam3d_tb2_kernel {STENCIL} f32 (Tb=2: 8 B per "
+                                    f"cell per launch = 2 updates)" if tb > 1
+                                    else f"ssam3d_halo_kernel {STENCIL} f32"),
                          "bytes_per_launch": 8 * cells_per_launch,
                          "mean_launch_ms": round(mean_ms, 4)},
             "e2e": e2e, "gpu_launches": int(nl.item()), "clocks": clk,
@@ -454,8 +474,21 @@ def kernel_suite(peak, sm_mhz):
             gc = n ** 3 * iters / ms / 1e6
             out[f"stencil3d_{name}_{dt}_512_x{iters}"] = {
                 "gcells": round(gc, 2), "hbm_gbs_equiv": round(gc * 2 * sz, 1),
-                "hbm_frac": round(gc * 2 * sz / peak, 4), "ms": round(ms, 3)}
+                "hbm_frac": round(gc * 2 * sz / peak, 4), "ms": round(ms, 3),
+                "tb": dev.stencil3d_tb_max(st, npdt) if name == "3d7pt" else 1}
         del a, bb
+    # the headline slab with two fused sweeps per HBM pass (engine3d_tb.cuh)
+    a = torch.empty((NZ_PER_GPU + 2, NY, NX), dtype=torch.float32, device="cuda")
+    dev.fill_random(a, 0)
+    bb = a.clone()
+    st = ssam.convert_stencil(ssam.make_benchmark_stencil("3d7pt"), np.float32)
+    ms = timed(lambda: dev.stencil3d_tb(a, bb, st, 2), 5)
+    gc = 2 * (NX - 2) * (NY - 2) * NZ_PER_GPU / ms / 1e6
+    out[f"stencil3d_3d7pt_f32_{NX}x{NY}x{NZ_PER_GPU + 2}_tb2"] = {
+        "gcells": round(gc, 2), "hbm_gbs": round(gc * 4, 1), "hbm_frac": round(gc * 4 / peak, 4),
+        "hbm_gbs_equiv": round(gc * 8, 1), "ms": round(ms, 3), "tb": 2,
+        "note": "cell-updates/s of one fused 2-sweep launch (8 B/cell per launch)"}
+    del a, bb
     # 1D (kernels.hpp:390-447): conv1d 9 taps and the one-pass scan over 2^28 elements
     # (1 GiB fp32, far above L2), HBM-bound at 2 * sizeof(T) bytes per element.
     n1 = 1 << 28
@@ -483,6 +516,8 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--iters", type=int, default=100, help="sweeps per step")
+    ap.add_argument("--tb", type=int, default=1,
+                    help="temporal block depth of the headline sweeps (1 or 2)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

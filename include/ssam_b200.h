@@ -173,10 +173,15 @@ int ssam_b200_stencil2d_tb_max(int dtype, const ssam_stencil* st);
 int ssam_b200_stencil3d_sweep(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
                               int z_begin, int z_end, const ssam_stencil* st, void* stream);
 
-/* tb fused 3D sweeps (temporal blocking, tb = 2 for order-1 stencils) over
- * the whole grid; SSAM_ERR_INVALID_ARGUMENT if no fused kernel exists.
- * d_out's ring must equal d_in's.  _tb_max: deepest fused block (1 = none). */
+/* tb fused 3D sweeps (temporal blocking, tb = 2 for order-1 stencils):
+ * writes planes [z_begin, z_end) of the interior; planes outside
+ * [z_ring_lo, z_ring_hi) are the global ring and stay fixed (a whole grid
+ * passes k, nz-k; a z-slab with k*tb ghost planes its local bounds, which
+ * may lie outside the buffer).  Reads planes z_begin-k*tb .. z_end-1+k*tb.
+ * SSAM_ERR_INVALID_ARGUMENT if no fused kernel exists.  d_out's ring must
+ * equal d_in's.  _tb_max: deepest fused block (1 = none). */
 int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
+                           int z_begin, int z_end, int z_ring_lo, int z_ring_hi,
                            const ssam_stencil* st, int tb, void* stream);
 int ssam_b200_stencil3d_tb_max(int dtype, const ssam_stencil* st);
 

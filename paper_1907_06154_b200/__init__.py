@@ -122,7 +122,7 @@ _sig("ssam_b200_stencil2d_sweep", [_i, _p, _p, _i, _i, _i, _i, _PS, _p])
 _sig("ssam_b200_stencil2d_tb", [_i, _p, _p, _i, _i, _PS, _i, _p])
 _sig("ssam_b200_stencil2d_tb_max", [_i, _PS])
 _sig("ssam_b200_stencil3d_sweep", [_i, _p, _p, _i, _i, _i, _i, _i, _PS, _p])
-_sig("ssam_b200_stencil3d_tb", [_i, _p, _p, _i, _i, _i, _PS, _i, _p])
+_sig("ssam_b200_stencil3d_tb", [_i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _PS, _i, _p])
 _sig("ssam_b200_stencil3d_tb_max", [_i, _PS])
 _sig("ssam_b200_stencil2d_run", [_i, _p, _p, _i, _i, _PS, _i, _i, _p, C.POINTER(_p)])
 _sig("ssam_b200_stencil3d_run", [_i, _p, _p, _i, _i, _i, _PS, _i, _p, C.POINTER(_p)])

@@ -402,7 +402,7 @@ cudaError_t run3d(T* a, T* b, int nx, int ny, int nz, const StencilDesc<T>& d, i
     int depth = 1;
     if (tb > 1 && iters - done >= tb) {
       depth = tb;
-      e = stencil3d_tb<T>(cur, nxt, nx, ny, nz, d, tb, s);
+      e = stencil3d_tb<T>(cur, nxt, nx, ny, nz, 0, nz, d.order, nz - d.order, d, tb, s);
       if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         depth = 1;
@@ -1033,6 +1033,7 @@ int ssam_b200_gather_stencil(int dtype, const void* in, int nx, int ny, int nz,
 }
 
 int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
+                           int z_begin, int z_end, int z_ring_lo, int z_ring_hi,
                            const ssam_stencil* st, int tb, void* stream) {
   g_err.clear();
   if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
@@ -1042,8 +1043,8 @@ int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int
   cudaError_t e = cudaErrorNotSupported;
   const cudaStream_t s = as_stream(stream);
   switch (dtype) {
-    case 0: e = stencil3d_tb<float>(static_cast<const float*>(d_in), static_cast<float*>(d_out), nx, ny, nz, make_desc<float>(st), tb, s); break;
-    case 1: e = stencil3d_tb<double>(static_cast<const double*>(d_in), static_cast<double*>(d_out), nx, ny, nz, make_desc<double>(st), tb, s); break;
+    case 0: e = stencil3d_tb<float>(static_cast<const float*>(d_in), static_cast<float*>(d_out), nx, ny, nz, z_begin, z_end, z_ring_lo, z_ring_hi, make_desc<float>(st), tb, s); break;
+    case 1: e = stencil3d_tb<double>(static_cast<const double*>(d_in), static_cast<double*>(d_out), nx, ny, nz, z_begin, z_end, z_ring_lo, z_ring_hi, make_desc<double>(st), tb, s); break;
     default: break;
   }
   if (e == cudaErrorNotSupported) {

@@ -38,6 +38,7 @@ struct Ssam3DParams {
   int vec_ok;
   int cta_sx;       // TMA kernel: adjacent x-strips per CTA (sharing one box)
   int zfast;        // TMA kernels: grid is (x, z-segment, y-group) instead of (x, y, z)
+  int zr_lo, zr_hi; // fused (Tb > 1) kernel: planes outside [zr_lo, zr_hi) are global ring
   T coef[CAP];      // coef[(l*M + j)*M + t], l = dz+K, j = dx+K, t = dy+K
 };
 

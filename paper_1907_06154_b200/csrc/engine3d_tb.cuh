@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256)
         if (m >= n_mid) break;
         take(m + 2 * K, pl[(ph + NPL - 1) % NPL]);
         const int z = z0 - K + m;
-        const bool zring = z < p.ring || z >= p.nz - p.ring;
+        const bool zring = z < p.zr_lo || z >= p.zr_hi;
         const int s = m % DI;
         if (m >= DI) mbar_wait(smem_u32(&mid_empty[s]), ((m / DI) - 1) & 1);
         T* dst = mid_ring + s * (G::MID_SLOT / sizeof(T)) + Q * lane;

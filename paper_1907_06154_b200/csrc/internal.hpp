@@ -59,11 +59,13 @@ template <class T>
 cudaError_t stencil3d_sweep(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin,
                             int z_end, const StencilDesc<T>& st, cudaStream_t s);
 
-// Tb fused 3D sweeps (temporal blocking) over the whole grid.  Returns
-// cudaErrorNotSupported when no fused kernel exists (the caller then sweeps).
+// Tb fused 3D sweeps (temporal blocking) writing planes [z_begin, z_end) of
+// the interior; planes outside [zr_lo, zr_hi) are the global ring (kept
+// fixed), so a z-slab with k*Tb ghost planes passes its local bounds.
+// Returns cudaErrorNotSupported when no fused kernel exists.
 template <class T>
-cudaError_t stencil3d_tb(const T* d_in, T* d_out, int nx, int ny, int nz,
-                         const StencilDesc<T>& st, int tb, cudaStream_t s);
+cudaError_t stencil3d_tb(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
+                         int zr_lo, int zr_hi, const StencilDesc<T>& st, int tb, cudaStream_t s);
 int stencil3d_tb_max(int dtype, int order);
 
 // ---- direct-gather kernels (generic path: any order / tap set) -------------

@@ -104,13 +104,15 @@ int stencil3d_tb_max(int dtype, int order) {
 }
 
 template <class T, class Mask>
-cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, const T* coef,
-                        cudaStream_t s) {
+cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
+                        int zr_lo, int zr_hi, const T* coef, cudaStream_t s) {
   constexpr int K = 1, M = 3, Q = Lanes<T>::Q, RY = 4, CAP = 27;
   using G = Tb3Geom<T, Q, K, RY>;
   constexpr int VQ = 16 / sizeof(T);
   if (nx % VQ != 0 || !aligned16(d_in) || !aligned16(d_out)) return cudaErrorNotSupported;
-  const int zb = K, ze = nz - K, yrows = ny - 2 * K;
+  // outputs [z_begin, z_end) within the global interior [zr_lo, zr_hi); the
+  // fused pair reads planes z_begin-2K .. z_end-1+2K (a slab's ghosts)
+  const int zb = std::max(z_begin, zr_lo), ze = std::min(z_end, zr_hi), yrows = ny - 2 * K;
   if (ze <= zb || yrows <= 0 || nx - 2 * K <= 0) return cudaSuccess;
   Ssam3DTmaParams<T, CAP> P;
   std::memset(&P, 0, sizeof(P));
@@ -133,6 +135,8 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, const T
   p.zseg = zseg;
   p.z_begin = zb;
   p.z_end = ze;
+  p.zr_lo = zr_lo;
+  p.zr_hi = zr_hi;
   p.cta_sx = 1;
   std::memcpy(p.coef, coef, sizeof(T) * M * M * M);
   const dim3 grid(p.nstrips, (yrows + G::ROWS2 - 1) / G::ROWS2, (zrows + zseg - 1) / zseg);
@@ -148,30 +152,35 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, const T
 }
 
 template <class T>
-cudaError_t stencil3d_tb_impl(const T* d_in, T* d_out, int nx, int ny, int nz,
-                              const StencilDesc<T>& st, int tb, cudaStream_t s) {
+cudaError_t stencil3d_tb_impl(const T* d_in, T* d_out, int nx, int ny, int nz, int zb, int ze,
+                              int rlo, int rhi, const StencilDesc<T>& st, int tb, cudaStream_t s) {
   if (tb != 2 || st.order != 1 || std::is_same<T, long long>::value) return cudaErrorNotSupported;
   const std::vector<T> coef = dense3d_coef(st);
   switch (classify3d(st.taps, 1)) {
-    case Shape3D::star: return launch_tb3d<T, StarMask3<1>>(d_in, d_out, nx, ny, nz, coef.data(), s);
-    case Shape3D::poisson: return launch_tb3d<T, PoissonMask3>(d_in, d_out, nx, ny, nz, coef.data(), s);
-    default: return launch_tb3d<T, DenseMask3>(d_in, d_out, nx, ny, nz, coef.data(), s);
+    case Shape3D::star:
+      return launch_tb3d<T, StarMask3<1>>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), s);
+    case Shape3D::poisson:
+      return launch_tb3d<T, PoissonMask3>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), s);
+    default:
+      return launch_tb3d<T, DenseMask3>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), s);
   }
 }
 
 template <>
-cudaError_t stencil3d_tb<float>(const float* i, float* o, int nx, int ny, int nz,
-                                const StencilDesc<float>& st, int tb, cudaStream_t s) {
-  return stencil3d_tb_impl<float>(i, o, nx, ny, nz, st, tb, s);
+cudaError_t stencil3d_tb<float>(const float* i, float* o, int nx, int ny, int nz, int zb, int ze,
+                                int rlo, int rhi, const StencilDesc<float>& st, int tb,
+                                cudaStream_t s) {
+  return stencil3d_tb_impl<float>(i, o, nx, ny, nz, zb, ze, rlo, rhi, st, tb, s);
 }
 template <>
-cudaError_t stencil3d_tb<double>(const double* i, double* o, int nx, int ny, int nz,
-                                 const StencilDesc<double>& st, int tb, cudaStream_t s) {
-  return stencil3d_tb_impl<double>(i, o, nx, ny, nz, st, tb, s);
+cudaError_t stencil3d_tb<double>(const double* i, double* o, int nx, int ny, int nz, int zb,
+                                 int ze, int rlo, int rhi, const StencilDesc<double>& st, int tb,
+                                 cudaStream_t s) {
+  return stencil3d_tb_impl<double>(i, o, nx, ny, nz, zb, ze, rlo, rhi, st, tb, s);
 }
 template <>
-cudaError_t stencil3d_tb<long long>(const long long*, long long*, int, int, int,
-                                    const StencilDesc<long long>&, int, cudaStream_t) {
+cudaError_t stencil3d_tb<long long>(const long long*, long long*, int, int, int, int, int, int,
+                                    int, const StencilDesc<long long>&, int, cudaStream_t) {
   return cudaErrorNotSupported;
 }
 

@@ -96,12 +96,19 @@ def stencil3d_sweep(d_in, d_out, st: Stencil, z_begin: int = 0, z_end: Optional[
                                           _s(stream)))
 
 
-def stencil3d_tb(d_in, d_out, st: Stencil, tb: int, stream=None) -> None:
-    """tb fused 3D sweeps (order-1 stencils, tb = 2); d_out's ring must equal d_in's."""
+def stencil3d_tb(d_in, d_out, st: Stencil, tb: int, z_begin: int = 0,
+                 z_end: Optional[int] = None, z_ring_lo: Optional[int] = None,
+                 z_ring_hi: Optional[int] = None, stream=None) -> None:
+    """tb fused 3D sweeps (order-1 stencils, tb = 2) writing planes [z_begin, z_end);
+    planes outside [z_ring_lo, z_ring_hi) (default: the buffer's own ring) stay fixed."""
     code = _code(d_in)
     nz, ny, nx = d_in.shape
     sa = _StencilArgs(st, _np_dtype(code))
+    k = st.order
     _raise(_lib.ssam_b200_stencil3d_tb(code, d_in.data_ptr(), d_out.data_ptr(), nx, ny, nz,
+                                       z_begin, nz if z_end is None else z_end,
+                                       k if z_ring_lo is None else z_ring_lo,
+                                       nz - k if z_ring_hi is None else z_ring_hi,
                                        sa.ref, tb, _s(stream)))
 
 

@@ -18,6 +18,12 @@ Overlap (per sweep): the 2*ghost boundary planes are computed first, their
 exchange runs on a communication stream while the interior planes are
 computed, and the next sweep waits only for the receives.
 
+Temporal blocking (Tb fused sweeps per step, ssam_b200_stencil3d_tb): with
+ghost = k*Tb planes a rank can run Tb sweeps on its owned planes before it
+needs its neighbours' new planes, so the exchange happens once per Tb sweeps
+with the same plane count per message.  The global ring is passed to the
+fused kernel in local plane coordinates (`ring_bounds`).
+
 The exchange goes through torch.distributed (NCCL over NVLink on a B200 box,
 gloo on CPU for tests).  The sweep itself is pluggable so the CPU tests can
 drive the identical decomposition/exchange code with the oracle; in the
@@ -55,6 +61,10 @@ class Slab:
         hi = min(self.z_first + self.nz_own, self.nz_global - self.order)
         return self.local(lo), self.local(max(lo, hi))
 
+    def ring_bounds(self):
+        """Local plane range [lo, hi) of the GLOBAL interior (may lie outside the buffer)."""
+        return self.local(self.order), self.local(self.nz_global - self.order)
+
     def boundary_ranges(self):
         """(low, high) boundary plane ranges whose results neighbours need."""
         lo, hi = self.compute_range()
@@ -78,14 +88,20 @@ def decompose(nz_global: int, world: int, rank: int, order: int, ghost: Optional
 
 
 SweepFn = Callable[[torch.Tensor, torch.Tensor, int, int], None]  # (cur, nxt, z_begin, z_end)
+# (cur, nxt, z_begin, z_end): `tb` fused sweeps writing nxt planes [z_begin, z_end)
 
 
 class SlabRunner:
     """Runs Jacobi sweeps on one rank's slab with neighbour halo exchange."""
 
-    def __init__(self, slab: Slab, sweep: SweepFn, group=None, comm_stream=None):
+    def __init__(self, slab: Slab, sweep: SweepFn, group=None, comm_stream=None,
+                 fused: Optional[SweepFn] = None, tb: int = 1):
+        if tb > 1 and (fused is None or slab.ghost < slab.order * tb):
+            raise ValueError(f"Tb={tb} needs a fused sweep and ghost >= {slab.order * tb}")
         self.slab = slab
         self.sweep = sweep
+        self.fused = fused
+        self.tb = tb
         self.group = group
         self.cuda = comm_stream is not None
         self.comm_stream = comm_stream
@@ -105,19 +121,21 @@ class SlabRunner:
             ops.append(dist.P2POp(dist.irecv, nxt[own_hi:own_hi + g], s.rank + 1, self.group))
         return dist.batch_isend_irecv(ops)
 
-    def step(self, cur: torch.Tensor, nxt: torch.Tensor) -> None:
-        """One sweep cur -> nxt including the halo exchange of nxt."""
+    def step(self, cur: torch.Tensor, nxt: torch.Tensor, fused: bool = False) -> None:
+        """One sweep (or self.tb fused sweeps) cur -> nxt including the halo
+        exchange of nxt."""
         s = self.slab
         lo, hi = s.compute_range()
         (bl0, bl1), (bh0, bh1) = s.boundary_ranges()
+        sweep = self.fused if fused else self.sweep
         if s.world == 1:
-            self.sweep(cur, nxt, lo, hi)
+            sweep(cur, nxt, lo, hi)
             return
         # boundary planes first ...
         if bl1 > bl0:
-            self.sweep(cur, nxt, bl0, bl1)
+            sweep(cur, nxt, bl0, bl1)
         if bh1 > max(bh0, bl1):  # thin slabs: the two boundary bands may touch
-            self.sweep(cur, nxt, max(bh0, bl1), bh1)
+            sweep(cur, nxt, max(bh0, bl1), bh1)
         if self.cuda:
             main = torch.cuda.current_stream()
             self.comm_stream.wait_stream(main)
@@ -125,14 +143,14 @@ class SlabRunner:
                 reqs = self._exchange(nxt)
             # ... interior while the halo is in flight
             if bh0 > bl1:
-                self.sweep(cur, nxt, bl1, bh0)
+                sweep(cur, nxt, bl1, bh0)
             for r in reqs:
                 r.wait()
             main.wait_stream(self.comm_stream)
         else:
             reqs = self._exchange(nxt)
             if bh0 > bl1:
-                self.sweep(cur, nxt, bl1, bh0)
+                sweep(cur, nxt, bl1, bh0)
             for r in reqs:
                 r.wait()
 
@@ -140,9 +158,12 @@ class SlabRunner:
         """iters sweeps; a holds the input, b must hold a copy of it (ring and
         ghosts).  Returns the buffer with the final generation."""
         cur, nxt = a, b
-        for _ in range(iters):
-            self.step(cur, nxt)
+        done = 0
+        while done < iters:
+            fused = self.tb > 1 and iters - done >= self.tb
+            self.step(cur, nxt, fused)
             cur, nxt = nxt, cur
+            done += self.tb if fused else 1
         return cur
 
 

@@ -22,7 +22,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, shape, name, iters, q):
+def _worker(rank, world, port, shape, name, iters, q, tb=1):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -40,7 +40,7 @@ def _worker(rank, world, port, shape, name, iters, q):
         cf = np.asarray([t.coeff for t in st.taps])
         nz, ny, nx = shape
         k = st.order
-        slab = decompose(nz, world, rank, k)
+        slab = decompose(nz, world, rank, k, ghost=k * tb)
         full = orc.random_grid(shape, np.float64, 21)
         z0 = slab.z_first - slab.ghost
         local = np.zeros((slab.nz_local, ny, nx))
@@ -57,15 +57,27 @@ def _worker(rank, world, port, shape, name, iters, q):
             out = orc.stencil3d(sub, offs, cf, k, 1)
             nxt[zb:ze] = torch.from_numpy(out[k:k + (ze - zb)])
 
-        res = SlabRunner(slab, sweep).run(a, b, iters)
+        def fused(cur, nxt, zb, ze):
+            # tb sweeps; sweep j writes [zb - k*(tb-1-j), ze + k*(tb-1-j)) of the
+            # global interior -- what the fused kernel computes on the GPU
+            rlo, rhi = slab.ring_bounds()
+            src = cur
+            for j in range(tb):
+                w = k * (tb - 1 - j)
+                dst = nxt if j == tb - 1 else src.clone()
+                sweep(src, dst, max(zb - w, rlo), min(ze + w, rhi))
+                src = dst
+
+        res = SlabRunner(slab, sweep, fused=fused if tb > 1 else None, tb=tb).run(a, b, iters)
         own = res[slab.ghost:slab.ghost + slab.nz_own].numpy()
         q.put((rank, slab.z_first, own))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,name", [(2, "3d7pt"), (3, "3d13pt"), (2, "3d27pt")])
-def test_slab_matches_global_oracle(world, name):
+@pytest.mark.parametrize("world,name,tb", [(2, "3d7pt", 1), (3, "3d13pt", 1), (2, "3d27pt", 1),
+                                           (2, "3d7pt", 2), (3, "poisson", 2)])
+def test_slab_matches_global_oracle(world, name, tb):
     from oracle import Oracle
     import paper_1907_06154_b200 as ssam
     shape = (23, 11, 13)
@@ -73,7 +85,7 @@ def test_slab_matches_global_oracle(world, name):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, name, iters, q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, shape, name, iters, q, tb))
              for r in range(world)]
     for p in procs:
         p.start()
