@@ -353,15 +353,26 @@ __host__ __device__ constexpr size_t halo3d_bytes(int sx, int sy) {
          static_cast<size_t>(sx * sy) * 128;
 }
 
-// Two 256-thread CTAs per SM for the light fp32 star (fits 128 registers
-// without spills); heavier footprints keep their registers.
+// CTA size / residency targets of the halo kernel: two 256-thread CTAs per SM
+// for the light fp32 star (fits 128 registers without spills); the heavier
+// footprints run 128-thread CTAs, three per SM for fp32 order 1 (<= 170
+// registers).
+template <class T, int K, class Mask>
+__host__ __device__ constexpr bool halo3d_light() {
+  return sizeof(T) == 4 && K == 1 && Mask::has(0, 1, 1) && !Mask::has(0, 0, 1);
+}
+template <class T, int K, class Mask>
+__host__ __device__ constexpr int halo3d_max_threads() {
+  return halo3d_light<T, K, Mask>() ? 256 : 128;
+}
 template <class T, int K, class Mask>
 __host__ __device__ constexpr int halo3d_min_blocks() {
-  return (sizeof(T) == 4 && K == 1 && Mask::has(0, 1, 1) && !Mask::has(0, 0, 1)) ? 2 : 1;
+  return halo3d_light<T, K, Mask>() ? 2 : (sizeof(T) == 4 && K == 1 ? 3 : 1);
 }
 
 template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP>
-__global__ void __launch_bounds__(256, (halo3d_min_blocks<T, K, Mask>()))
+__global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
+                                  (halo3d_min_blocks<T, K, Mask>()))
     ssam3d_halo_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
   static_assert(K >= 1, "order-0 stencils have no chain");
   const Ssam3DParams<T, CAP>& p = P.p;
@@ -388,17 +399,6 @@ __global__ void __launch_bounds__(256, (halo3d_min_blocks<T, K, Mask>()))
   const int count = (z1 - z0) + 2 * K;
   const bool is_r = lane == 31;
 
-  // per-lane halo coefficients: lane 31 mirrors (dx -> -dx)
-  T hc[K][M][M];
-#pragma unroll
-  for (int m = 0; m < K; ++m)
-#pragma unroll
-    for (int l = 0; l < M; ++l)
-#pragma unroll
-      for (int t = 0; t < M; ++t)
-        hc[m][l][t] = Mask::has(m, t, l)
-                          ? (is_r ? p.coef[(l * M + (M - 1 - m)) * M + t] : p.coef[(l * M + m) * M + t])
-                          : T(0);
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw);
@@ -479,7 +479,9 @@ __global__ void __launch_bounds__(256, (halo3d_min_blocks<T, K, Mask>()))
           for (int m = 0; m < K; ++m) {
 #pragma unroll
             for (int c = K - 1; c >= m; --c) {
-              T cp = T(0);
+              // both sides' colparts with constant-bank weights (lane 31
+              // mirrors dx -> -dx); each lane keeps its own side's
+              T cl = T(0), cr = T(0);
               bool any = false;
 #pragma unroll
               for (int l = 0; l < M; ++l)
@@ -487,9 +489,13 @@ __global__ void __launch_bounds__(256, (halo3d_min_blocks<T, K, Mask>()))
                 for (int t = 0; t < M; ++t)
                   if (Mask::has(m, t, l)) {
                     const T v = hp[(ph + l) % NPL][r + t][c];
-                    cp = any ? fma_t(hc[m][l][t], v, cp) : hc[m][l][t] * v;
+                    const T wl = p.coef[(l * M + m) * M + t];
+                    const T wr = p.coef[(l * M + (M - 1 - m)) * M + t];
+                    cl = any ? fma_t(wl, v, cl) : wl * v;
+                    cr = any ? fma_t(wr, v, cr) : wr * v;
                     any = true;
                   }
+              const T cp = is_r ? cr : cl;
               if (m == 0)
                 h[c] = any ? cp : T(0);
               else

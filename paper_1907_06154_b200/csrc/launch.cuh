@@ -155,9 +155,9 @@ inline int cta_strips_3d() {
 // The halo-lane 3D kernel (engine3d.cuh) exists for order >= 1 x-symmetric
 // masks except the 125-tap box.  Measured (B200, 512^3 and 2048^2x514, vs
 // the aligned-plan kernel, bit-identical): fp32 3d7pt +12% / +1.3%, 3d13pt
-// fp32 +22%, fp64 +8%; the 27-point box, Poisson and fp64 3d7pt lose
-// 3-17% (their extra halo registers cost occupancy), so they keep the
-// aligned plan.  SSAM_B200_3D_HALO=0/1 forces it off/on where it exists.
+// fp32 +22%, fp64 +8%, fp32 Poisson +7% (halo weights as constant-bank
+// operands, 3 CTAs/SM); the fp32 27-point box is even and the fp64 order-1
+// footprints lose 8-17% (registers), so they keep the aligned plan.  SSAM_B200_3D_HALO=0/1 forces it off/on where it exists.
 inline int halo_mode_3d() {
   static const int v = [] {
     const char* e = std::getenv("SSAM_B200_3D_HALO");
@@ -168,7 +168,8 @@ inline int halo_mode_3d() {
 template <class T, int K, class Mask>
 constexpr bool halo_default_3d() {
   return std::is_same<Mask, StarMask3<2>>::value ||
-         (sizeof(T) == 4 && std::is_same<Mask, StarMask3<1>>::value);
+         (sizeof(T) == 4 && (std::is_same<Mask, StarMask3<1>>::value ||
+                             std::is_same<Mask, PoissonMask3>::value));
 }
 
 // CTA order of the TMA kernels.  The hardware launches blockIdx.x fastest,
@@ -244,6 +245,7 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
       p.nstrips = (a.nx - K + p.V - 1) / p.V;
       const bool light = std::is_same<Mask, StarMask3<1>>::value;
       int wpb = cta_warps_3d() ? cta_warps_3d() : (light ? 8 : 4);
+      wpb = std::min(wpb, halo3d_max_threads<T, K, Mask>() / 32);  // the kernel's launch bound
       const int want_sx = cta_strips_3d() ? cta_strips_3d() : (light ? 2 : 1);
       int sx = (want_sx >= 2 && p.nstrips >= 2) ? 2 : 1;
       auto fits = [&](int w, int x) {
