@@ -130,7 +130,12 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
   p.ring = K;
   p.vec_ok = 1;
   const int zrows = ze - zb;
-  int zseg = std::min(zrows, 32);
+  // Long z-segments amortise the 4-plane prologue of the fused pair (2048^2
+  // x 514: 908 / 991 / 1028 / 1053 GCells/s at 16 / 32 / 64 / 128 planes),
+  // as long as the grid keeps about four waves of CTAs (512^3 wants 32-64).
+  const long long xy_ctas = static_cast<long long>(p.nstrips) * ((yrows + G::ROWS2 - 1) / G::ROWS2);
+  int zseg = std::min(zrows, 128);
+  while (zseg > 16 && xy_ctas * ((zrows + zseg - 1) / zseg) < 4 * 2 * kSMs) zseg /= 2;
   if (const char* e = std::getenv("SSAM_B200_3D_TB_ZSEG")) zseg = std::max(4, std::atoi(e));
   p.zseg = zseg;
   p.z_begin = zb;
