@@ -308,7 +308,11 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_slab(args, slab, st, world, rank)
+        try:
+            e2e = e2e_slab(args, slab, st, world, rank)
+        except Exception as ex:  # e.g. pinned host memory exhausted on a big box
+            e2e = {"value": None, "unit": "GCells/s", "error": f"{type(ex).__name__}: {ex}"[:300]}
+            torch.cuda.empty_cache()
 
     kernels = None
     cpu = None
