@@ -27,9 +27,12 @@ std::vector<T> conv_coef(const T* w, int m, int n) {
 
 // Columns per lane: two 16-byte chunks for short fp32 filters (halves the
 // per-cell shuffle and loop overhead), one chunk otherwise.
+#ifndef SSAM_CONV_Q8_MAXN
+#define SSAM_CONV_Q8_MAXN 4
+#endif
 template <class T>
 constexpr int conv_q(int n) {
-  return sizeof(T) == 4 ? (n <= 4 ? 8 : 4) : 2;
+  return sizeof(T) == 4 ? (n <= SSAM_CONV_Q8_MAXN ? 8 : 4) : 2;
 }
 
 // Square filters with K >= SSAM_B200_CONV_FMA (default 6; 0 = never) take the
@@ -42,7 +45,8 @@ inline int conv_fma_min_k() {
   return v;
 }
 
-template <class T, int Q, int NR, int MC, int RY, bool EXACT, int CAP, class Mask = DenseMask>
+template <class T, int Q, int NR, int MC, int RY, bool EXACT, int CAP, class Mask = DenseMask,
+          bool CHAIN1 = false>
 cudaError_t launch_fma2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int RB = RY > 4 ? RY : 4;
   constexpr int D = 3;
@@ -73,7 +77,7 @@ cudaError_t launch_fma2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   p.ring = a.ring;
   p.vec_ok = 1;
   std::memcpy(p.coef, a.coef, sizeof(T) * a.M * NR);
-  auto kern = ssam2d_fma_kernel<T, Q, NR, MC, Mask, RY, RB, D, EXACT, CAP>;
+  auto kern = ssam2d_fma_kernel<T, Q, NR, MC, Mask, RY, RB, D, EXACT, CAP, CHAIN1>;
   const size_t smem = fma2d_smem<T, Q, NR, RB, D, EXACT>(kWarpsPerBlock, a.M);
   const int gx = (p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock;
   const dim3 grid(gx, (rows + p.seg - 1) / p.seg);

@@ -65,7 +65,8 @@ __host__ __device__ constexpr size_t fma2d_smem(int warps, int m) {
          static_cast<size_t>(m) * ((NR * sizeof(T) + 15) / 16 * 16);
 }
 
-template <class T, int Q, int NR, int MC, class Mask, int RY, int RB, int D, bool EXACT, int CAP>
+template <class T, int Q, int NR, int MC, class Mask, int RY, int RB, int D, bool EXACT, int CAP,
+          bool CHAIN1 = false>
 __global__ void __launch_bounds__(128)
     ssam2d_fma_kernel(const __grid_constant__ Ssam2DTmaParams<T, CAP> P) {
   static_assert(RB % RY == 0, "passes never straddle boxes");
@@ -219,6 +220,58 @@ __global__ void __launch_bounds__(128)
 
     T acc[RY][Q];
     const int R = (M - 1) / 2, L = M - 1 - R;
+    if constexpr (CHAIN1) {
+      // Single chain (stencils): every tap FMAs straight into the shifted
+      // partial sum -- the reference simulator's own stage order (one MAD per
+      // tap, a shift between columns, kernels.hpp:111-159) without the
+      // column-partial FMUL / FADD pair, which for 1-tap star columns doubled
+      // the work.
+      auto colfma = [&](const T (&c)[NRP], int j, int r, T (&a)[Q]) {
+#pragma unroll
+        for (int t = 0; t < NR; ++t)
+          if (Mask::has(j, t)) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) a[q] = fma_t(c[t], win[r + t][q], a[q]);
+          }
+      };
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[r][q] = T(0);
+#pragma unroll(UNROLL ? 20 : 1)
+      for (int j = 0; j <= L; ++j) {
+        T c[NRP];
+        load_col(j, c);
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          if (j > 0) shift_up1<T, Q>(acc[r]);
+          colfma(c, j, r, acc[r]);
+        }
+      }
+      if (R > 0) {
+        T accr[RY][Q];
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) accr[r][q] = T(0);
+#pragma unroll(UNROLL ? 20 : 1)
+        for (int j = M - 1; j > L; --j) {
+          T c[NRP];
+          load_col(j, c);
+#pragma unroll
+          for (int r = 0; r < RY; ++r) {
+            if (j < M - 1) shift_down1<T, Q>(accr[r]);
+            colfma(c, j, r, accr[r]);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          shift_down1<T, Q>(accr[r]);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[r][q] += accr[r][q];
+        }
+      }
+    } else {
     // left chain: columns 0..L flow up (shfl_up) into the output lane
     {
       T c[NRP];
@@ -272,6 +325,7 @@ __global__ void __launch_bounds__(128)
         for (int q = 0; q < Q; ++q) acc[r][q] += accr[r][q];
       }
     }
+    }  // two-level chain
     const int y = y0 + pass * RY;
 #pragma unroll
     for (int r = 0; r < RY; ++r) {

@@ -40,13 +40,27 @@ inline bool st2d_fma_enabled() {
   return v;
 }
 
+// Tall stencils accumulate in one FMA chain per output (CHAIN1, the
+// reference simulator's stage order); SSAM_B200_ST2D_CHAIN1=0 keeps the
+// conv-style two-level order.
+inline bool st2d_chain1() {
+  static const bool v = [] {
+    const char* e = std::getenv("SSAM_B200_ST2D_CHAIN1");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 template <class T, int Q, int K, class Mask>
 cudaError_t st2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
   constexpr int QQ = st_q<T>(K);
   if constexpr (K >= 4 && !std::is_same<T, long long>::value) {
-    if (st2d_fma_enabled() && fma_eligible(a))
-      return launch_fma2d<T, QQ, M, M, 4, false, M * M, Mask>(a, s);
+    if (st2d_fma_enabled() && fma_eligible(a)) {
+      if (st2d_chain1())
+        return launch_fma2d<T, QQ, M, M, 4, false, M * M, Mask, true>(a, s);
+      return launch_fma2d<T, QQ, M, M, 4, false, M * M, Mask, false>(a, s);
+    }
   }
   return launch_ssam2d<T, QQ, M, M, Mask, pf_rows(M), M * M>(a, s);
 }
