@@ -57,9 +57,10 @@ cudaError_t st2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int QQ = st_q<T>(K);
   if constexpr (K >= 4 && !std::is_same<T, long long>::value) {
     if (st2d_fma_enabled() && fma_eligible(a)) {
+      constexpr int QW = QQ, RYW = 4;  // Q = 8 / RY = 2 measured no better (higher registers)
       if (st2d_chain1())
-        return launch_fma2d<T, QQ, M, M, 4, false, M * M, Mask, true>(a, s);
-      return launch_fma2d<T, QQ, M, M, 4, false, M * M, Mask, false>(a, s);
+        return launch_fma2d<T, QW, M, M, RYW, false, M * M, Mask, true>(a, s);
+      return launch_fma2d<T, QW, M, M, RYW, false, M * M, Mask, false>(a, s);
     }
   }
   return launch_ssam2d<T, QQ, M, M, Mask, pf_rows(M), M * M>(a, s);
