@@ -188,6 +188,27 @@ def run_reference_arm(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def backend() -> str:
+    """NCCL in production; SSAM_BENCH_BACKEND=gloo runs the N > 1 flow on fewer GPUs
+    (ranks share devices, halos staged through host memory) to test it on one B200."""
+    return os.environ.get("SSAM_BENCH_BACKEND", "nccl")
+
+
+def rank_device(local_rank: int) -> int:
+    import torch
+    return local_rank % max(1, torch.cuda.device_count())
+
+
+def reduce_host(x: float, op: str) -> float:
+    """Max / sum of a scalar over ranks (device tensor for NCCL, host for gloo)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64,
+                     device="cuda" if backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def workload_config(world: int, args):
     return {"workload": f"{STENCIL} f32 {NX}x{NY}x({NZ_PER_GPU}*N) z-slab, NVLink halo exchange",
             "stencil": STENCIL, "nx": NX, "ny": NY, "nz": NZ_PER_GPU * world,
@@ -209,7 +230,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     from paper_1907_06154_b200 import device as dev
     from paper_1907_06154_b200.slab import SlabRunner, decompose, fill_slab
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(rank_device(local_rank))
     peak, peak_kind, sm_max_nominal = load_peaks()
     st = ssam.convert_stencil(ssam.make_benchmark_stencil(STENCIL), np.float32)
     k = st.order
@@ -260,7 +281,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     barrier()
 
-    clocks = ClockSampler(torch.cuda.current_device())
+    clocks = ClockSampler(torch.cuda.current_device())  # nvidia-smi index = CUDA index here
     clocks.start()
     time.sleep(0.3)
     n_launch0 = ssam.launch_count()
@@ -279,12 +300,10 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     elapsed_ms = t_start.elapsed_time(t_end)
     launches = ssam.launch_count() - n_launch0
 
-    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
-    nl = torch.tensor([launches], dtype=torch.float64, device="cuda")
+    max_ms, n_launches = elapsed_ms, float(launches)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(nl, op=dist.ReduceOp.SUM)
-    max_ms = float(t.item())
+        max_ms = reduce_host(elapsed_ms, "max")
+        n_launches = reduce_host(float(launches), "sum")
     total_cells = NX * NY * NZ_PER_GPU * world * args.iters * args.steps
     value = total_cells / (max_ms / 1e3) / 1e9
 
@@ -344,7 +363,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
                                     else f"ssam3d_halo_kernel {STENCIL} f32"),
                          "bytes_per_launch": 8 * cells_per_launch,
                          "mean_launch_ms": round(mean_ms, 4)},
-            "e2e": e2e, "gpu_launches": int(nl.item()), "clocks": clk,
+            "e2e": e2e, "gpu_launches": int(n_launches), "clocks": clk,
             "cpu_baseline": cpu, "kernels": kernels,
         }
         print(json.dumps(line), flush=True)
@@ -400,11 +419,8 @@ def e2e_slab(args, slab, st, world, rank):
     for _ in range(steps):
         one()
     dt = time.perf_counter() - t0
-    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
     if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dt = float(t.item())
+        dt = reduce_host(dt, "max")
     cells = NX * NY * NZ_PER_GPU * world * args.iters * steps
     nbytes = nzl * NY * NX * 4
     return {"value": round(cells / dt / 1e9, 3), "unit": "GCells/s",
@@ -544,8 +560,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev_index = rank_device(local_rank)
+        torch.cuda.set_device(dev_index)
+        if backend() == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend())
     try:
         run_ours(args, rank, world, local_rank)
     finally:
