@@ -91,9 +91,9 @@ __device__ __forceinline__ void row_chain(const T (&pl)[NPL][NROW][Q], int ph, i
 }
 
 // Geometry shared by host and device.
-template <class T, int Q, int K, int RY>
+template <class T, int Q, int K, int RY, int SY_ = 4>
 struct Tb3Geom {
-  static constexpr int SY = 4;                        // stage-2 warps (row groups)
+  static constexpr int SY = SY_;                      // stage-2 warps (row groups)
   static constexpr int ROWS2 = SY * RY;               // output rows per CTA
   static constexpr int IROWS = ROWS2 + 2 * K;         // intermediate rows (sweep-1 band)
   static constexpr int RY1 = (IROWS + SY - 1) / SY;   // sweep-1 rows per stage-1 warp
@@ -102,13 +102,15 @@ struct Tb3Geom {
   static constexpr int DZ = 4, DI = 4;                // input / intermediate ring depth
   static constexpr size_t IN_SLOT = (size_t(BROWS) * BW * sizeof(T) + 127) / 128 * 128;
   static constexpr size_t MID_SLOT = (size_t(IROWS) * BW * sizeof(T) + 127) / 128 * 128;
-  static constexpr size_t SMEM = DZ * IN_SLOT + DI * MID_SLOT + (2 * DZ + 2 * DI) * 8 + 256 * 4;
+  static constexpr int THREADS = 2 * SY * 32;          // SY sweep-1 + SY sweep-2 warps
+  static constexpr size_t SMEM =
+      DZ * IN_SLOT + DI * MID_SLOT + (2 * DZ + 2 * DI) * 8 + THREADS * 4;
 };
 
-template <class T, int Q, int K, class Mask, int RY, int CAP>
-__global__ void __launch_bounds__(256)
+template <class T, int Q, int K, class Mask, int RY, int CAP, int SY = 4>
+__global__ void __launch_bounds__(2 * SY * 32)
     ssam3d_tb2_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
-  using G = Tb3Geom<T, Q, K, RY>;
+  using G = Tb3Geom<T, Q, K, RY, SY>;
   constexpr int M = 2 * K + 1, NPL = M;
   constexpr int NROW1 = G::RY1 + 2 * K, NROW2 = RY + 2 * K;
   constexpr int BW = G::BW, DZ = G::DZ, DI = G::DI;

@@ -107,7 +107,10 @@ template <class T, class Mask>
 cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
                         int zr_lo, int zr_hi, const T* coef, cudaStream_t s) {
   constexpr int K = 1, M = 3, Q = Lanes<T>::Q, RY = 4, CAP = 27;
-  using G = Tb3Geom<T, Q, K, RY>;
+  // 8-warp CTAs for the light star; the heavier masks hold ~160 registers
+  // and run 4-warp CTAs (three resident per SM instead of one).
+  constexpr int SY = std::is_same<Mask, StarMask3<1>>::value ? 4 : 2;
+  using G = Tb3Geom<T, Q, K, RY, SY>;
   constexpr int VQ = 16 / sizeof(T);
   if (nx % VQ != 0 || !aligned16(d_in) || !aligned16(d_out)) return cudaErrorNotSupported;
   // outputs [z_begin, z_end) within the global interior [zr_lo, zr_hi); the
@@ -148,10 +151,10 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
   cudaError_t e = make_tmap_2d(&P.tmap, d_in, sizeof(T), nx, static_cast<uint64_t>(ny) * nz,
                                sizeof(T) * nx, G::BW, G::BROWS);
   if (e != cudaSuccess) return e;
-  auto kern = ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP>;
+  auto kern = ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP, SY>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
-  kern<<<grid, 256, G::SMEM, s>>>(P);
+  kern<<<grid, G::THREADS, G::SMEM, s>>>(P);
   note_launch();
   return cudaGetLastError();
 }
