@@ -284,8 +284,10 @@ template cudaError_t stencil2d_tb<long long>(const long long*, long long*, int, 
 // Deepest fused depth for automatic scheduling (1 = none).
 int stencil2d_tb_max(int dtype, int order, bool star) {
   if (dtype == 2 || !star) return 1;
-  if (order == 1) return 4;  // TB=8 is compiled but measured slower (register pressure)
-  if (order == 2) return 4;
+  // Measured x100 on 8192^2 (GCells/s, Tb = 1/2/4/8): 2d5pt f32 664/964/1420/1411,
+  // f64 349/595/808/641; 2d9pt f32 661/874/933/-, f64 350/528/476/-.
+  if (order == 1) return 4;  // TB=8 is compiled but no faster (register pressure)
+  if (order == 2) return dtype == 1 ? 2 : 4;
   return 1;
 }
 
