@@ -167,6 +167,19 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* tmap, int 
       : "memory");
 }
 
+// Programmatic dependent launch (sm_90+): a grid launched with the
+// programmatic-serialization attribute may start while its predecessor
+// drains.  griddep_wait() blocks until the predecessor grid has completed
+// and its memory is visible -- every kernel calls it before its first
+// global read or write; griddep_launch() lets the next grid be scheduled
+// into SMs this grid frees.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }

@@ -88,7 +88,8 @@ cudaError_t launch_fma2d(const Engine2DArgs<T>& a, cudaStream_t s) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(P);
+  e = launch_pdl(kern, grid, dim3(32 * kWarpsPerBlock), smem, s, P);
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
 }

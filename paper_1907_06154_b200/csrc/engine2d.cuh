@@ -267,6 +267,8 @@ __global__ void __launch_bounds__(128)
     fence_mbar_init();
   }
   __syncwarp();
+  griddep_wait();    // predecessor grid done (PDL launch)
+  griddep_launch();  // let the next grid fill SMs as this one drains
   const int count = (y1 - y0) + NR - 1;  // stream rows y0-U .. y1-1+D
   const int nbox = (count + RB - 1) / RB;
   auto issue = [&](int j) {

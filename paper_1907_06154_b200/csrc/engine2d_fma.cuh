@@ -130,6 +130,8 @@ __global__ void __launch_bounds__(128)
     fence_mbar_init();
   }
   __syncwarp();
+  griddep_wait();    // predecessor grid done (PDL launch)
+  griddep_launch();  // let the next grid fill SMs as this one drains
   const int npass = (y1 - y0 + RY - 1) / RY;
   const int nbox = (OFF + NR - 1) / RB + npass * RY / RB + ((npass * RY) % RB ? 1 : 0);
   // stream row s is image row y0 - U - OFF + s

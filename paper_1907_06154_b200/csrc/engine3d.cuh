@@ -238,6 +238,8 @@ __global__ void __launch_bounds__(256)
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_wait();    // predecessor grid done (PDL launch)
+  griddep_launch();  // let the next grid fill SMs as this one drains
   // Plane i of the stream (z = z0 - K + i): rows y_cta0-K .. of the
   // flattened (ny*nz)-row view; planes outside [0, nz) land outside -> zeros.
   auto issue = [&](int i) {
@@ -415,6 +417,8 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_wait();    // predecessor grid done (PDL launch)
+  griddep_launch();  // let the next grid fill SMs as this one drains
   auto issue = [&](int i) {
     const int s = i % DZ;
     if (i >= DZ) mbar_wait(smem_u32(&empty[s]), ((i / DZ) - 1) & 1);

@@ -151,6 +151,8 @@ __global__ void __launch_bounds__(2 * SY * 32)
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_wait();    // predecessor grid done (PDL launch)
+  griddep_launch();  // let the next grid fill SMs as this one drains
 
   if (stage1) {
     // ---- sweep 1: input planes -> intermediate band rows y_cta0-K .. ------

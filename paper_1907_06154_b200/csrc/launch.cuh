@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <utility>
 
 #include "engine2d.cuh"
 #include "engine3d.cuh"
@@ -15,6 +16,32 @@ namespace ssam_b200 {
 
 constexpr int kSMs = 148;          // B200: 2 dies x 74 SMs
 constexpr int kWarpsPerBlock = 4;  // 128-thread blocks
+
+// Launches with programmatic stream serialization (PDL) for the TMA kernels,
+// which all start with griddep_wait(): back-to-back sweeps overlap one
+// launch's ramp-up with the previous one's tail.  SSAM_B200_PDL=0 disables.
+inline bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SSAM_B200_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Lane plan for an M-column footprint, Q columns per lane (engine2d.cuh).
 // R = (M-1)/2, L = M-1-R.  Lane 0 starts at the Q-aligned column
@@ -37,8 +64,15 @@ inline bool aligned16(const void* p) { return (reinterpret_cast<std::uintptr_t>(
 
 // Rows streamed per warp: enough warps for ~2 waves of ~24 resident warps/SM,
 // but long enough that the NR-1 prologue rows stay a small overhead.
+inline int seg_warps_per_sm() {
+  static const int v = [] {
+    const char* e = std::getenv("SSAM_B200_2D_WARPS_PER_SM");
+    return e ? std::max(1, std::atoi(e)) : 48;
+  }();
+  return v;
+}
 inline int pick_seg(int rows, int nstrips, int nr) {
-  const long long target_warps = static_cast<long long>(kSMs) * 48;
+  const long long target_warps = static_cast<long long>(kSMs) * seg_warps_per_sm();
   long long segs = (target_warps + nstrips - 1) / nstrips;
   segs = std::max<long long>(1, std::min<long long>(segs, rows));
   int seg = static_cast<int>((rows + segs - 1) / segs);
@@ -114,7 +148,8 @@ cudaError_t launch_ssam2d(const Engine2DArgs<T>& a, cudaStream_t s) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
-    kern<<<grid, 32 * kWarpsPerBlock, smem, s>>>(P);
+    e = launch_pdl(kern, grid, dim3(32 * kWarpsPerBlock), smem, s, P);
+    if (e != cudaSuccess) return e;
   } else {
     ssam2d_kernel<T, Q, NR, MC, Mask, PF, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
   }
@@ -268,7 +303,8 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
       }
-      kern<<<grid, 32 * wpb, smem, s>>>(P);
+      e = launch_pdl(kern, grid, dim3(32 * wpb), smem, s, P);
+      if (e != cudaSuccess) return e;
       launched = true;
     }
   }
@@ -306,7 +342,8 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
     }
-    kern<<<grid, 32 * wpb, smem, s>>>(P);
+    e = launch_pdl(kern, grid, dim3(32 * wpb), smem, s, P);
+    if (e != cudaSuccess) return e;
   } else {
     const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
                     (zrows + zseg - 1) / zseg);

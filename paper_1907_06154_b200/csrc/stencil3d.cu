@@ -154,7 +154,8 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
   auto kern = ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP, SY>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
-  kern<<<grid, G::THREADS, G::SMEM, s>>>(P);
+  e = launch_pdl(kern, grid, dim3(G::THREADS), G::SMEM, s, P);
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
 }

@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
     fence_mbar_init();
   }
   __syncwarp();
+  griddep_wait();    // predecessor grid done (PDL launch)
+  griddep_launch();  // let the next grid fill SMs as this one drains
   const int yin0 = y0 - TB * K;                // first input row of the stream
   const int count = (y1 - y0) + 2 * TB * K;    // input rows yin0 .. y1-1+TB*K
   const int nbox = (count + RB - 1) / RB;
@@ -232,7 +234,9 @@ cudaError_t launch_tb(const T* in, T* out, int W, int H, const StencilDesc<T>& s
   if (e != cudaSuccess) return e;
   const size_t smem = static_cast<size_t>(kWarpsPerBlock) * D * (RB * 32 * Q * sizeof(T) + 8);
   const dim3 grid((p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock, (rows + p.seg - 1) / p.seg);
-  tb2d_kernel<T, Q, K, Mask, TB, RB, D, CAP><<<grid, 32 * kWarpsPerBlock, smem, s>>>(p);
+  e = launch_pdl(tb2d_kernel<T, Q, K, Mask, TB, RB, D, CAP>, grid, dim3(32 * kWarpsPerBlock), smem,
+                 s, p);
+  if (e != cudaSuccess) return e;
   note_launch();
   return cudaGetLastError();
 }

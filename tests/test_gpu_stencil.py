@@ -263,8 +263,8 @@ def test_temporal_blocking_matches_sweeps(cuda_lib, orc, name, dt):
     tdt = torch.float32 if dt == "f32" else torch.float64
     offs, cfs = taps_of(st)
     cf = np.asarray(cfs, NP[dt])
-    tbmax = dev.stencil2d_tb_max(st, NP[dt])
-    assert tbmax >= 4
+    tbmax = dev.stencil2d_tb_max(st, NP[dt])  # the automatic depth (2 or 4 here)
+    assert tbmax >= 2
     for (H, W) in ((260, 300), (97, 1024)):
         g = orc.random_grid((H, W), NP[dt], 5)
         for iters in (1, 3, 8, 13):
@@ -274,8 +274,8 @@ def test_temporal_blocking_matches_sweeps(cuda_lib, orc, name, dt):
             want = orc.stencil2d(g, offs, cf, st.order, iters)
             assert max_rel_err(single, want) <= TOL[np.dtype(NP[dt])]
             for tb in (2, 4, 8):
-                if tb > tbmax:
-                    continue
+                if tb == 8 and st.order > 1:
+                    continue  # compiled for order 1 only
                 a = torch.from_numpy(g).cuda()
                 b = a.clone()
                 got = dev.stencil2d_run(a, b, st, iters, tb=tb).cpu().numpy()
