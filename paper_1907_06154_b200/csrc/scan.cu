@@ -10,7 +10,7 @@
 // B200 shape: reduce-then-scan over 256 x 8 rows x 16-byte tiles.
 //   1. scan_reduce_kernel: one CTA per tile sums it (read n).
 //   2. scan_carry_kernel: one CTA turns the tile sums into exclusive tile
-//      prefixes (tiles / 1024 block scans; 32 K tiles for 2^28 fp32).
+//      prefixes (32 serial sums per thread, one block ladder per 32 K tiles).
 //   3. scan_tile_kernel: one CTA per tile scans it from its prefix (read n,
 //      write n).
 // Within a tile every warp owns rows of 32 x 16 bytes (coalesced 512-byte
@@ -90,7 +90,12 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
-// Exclusive prefix of the tile sums, 1024 at a time with a running carry.
+// Exclusive prefix of the tile sums: each of the 1024 threads scans 32
+// consecutive sums serially, one block-wide ladder joins the thread totals,
+// and a running carry links chunks of 32 K sums (one chunk up to 2^30 fp32
+// elements).
+constexpr int kCarryItems = 32;
+
 template <class T>
 __global__ void __launch_bounds__(kCarryThreads)
     scan_carry_kernel(const T* __restrict__ tile_sum, T* __restrict__ tile_prefix, int tiles) {
@@ -99,10 +104,16 @@ __global__ void __launch_bounds__(kCarryThreads)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_carry = T(0);
   __syncthreads();
-  for (int base = 0; base < tiles; base += kCarryThreads) {
-    const int i = base + threadIdx.x;
-    const T x = i < tiles ? tile_sum[i] : T(0);
-    T t = x;
+  for (long long base = 0; base < tiles; base += static_cast<long long>(kCarryThreads) * kCarryItems) {
+    const long long i0 = base + static_cast<long long>(threadIdx.x) * kCarryItems;
+    T v[kCarryItems];
+    T run = T(0);
+#pragma unroll
+    for (int k = 0; k < kCarryItems; ++k) {
+      v[k] = run;  // exclusive within the thread
+      run += i0 + k < tiles ? tile_sum[i0 + k] : T(0);
+    }
+    T t = run;
 #pragma unroll
     for (int d = 1; d < 32; d *= 2) {
       const T u = __shfl_up_sync(kFull, t, d);
@@ -120,13 +131,14 @@ __global__ void __launch_bounds__(kCarryThreads)
       s_warp[lane] = w;
     }
     __syncthreads();
-    const T carry = s_carry;
     T ex = __shfl_up_sync(kFull, t, 1);
     if (lane == 0) ex = T(0);
-    const T pre = carry + ((wid > 0 ? s_warp[wid - 1] : T(0)) + ex);
-    if (i < tiles) tile_prefix[i] = pre;
+    const T pre = s_carry + ((wid > 0 ? s_warp[wid - 1] : T(0)) + ex);
+#pragma unroll
+    for (int k = 0; k < kCarryItems; ++k)
+      if (i0 + k < tiles) tile_prefix[i0 + k] = pre + v[k];
     __syncthreads();
-    if (threadIdx.x == kCarryThreads - 1) s_carry = pre + x;
+    if (threadIdx.x == kCarryThreads - 1) s_carry = pre + run;
     __syncthreads();
   }
 }
