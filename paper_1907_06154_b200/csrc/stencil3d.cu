@@ -95,11 +95,11 @@ inline int tb3d_max_env() {
 }
 
 // Measured (B200, bit-identical to two sweeps): 3d7pt fp32 +23% at 512^3,
-// +27% at 2048^2 x 130 over two single sweeps.  The heavier footprints and
-// fp64 carry 150-210 registers per thread in the fused kernel and lose
-// (poisson / 3d27pt fp32 -40%), so only the fp32 7-point star fuses.
+// +27..35% at 2048^2; fp64 (4-warp CTAs) +12% at 512^3, +21% at 2048^2 x 130.
+// The heavier footprints are compute-bound already and lose (poisson /
+// 3d27pt -20..30%), so only the 7-point star fuses (run3d checks the shape).
 int stencil3d_tb_max(int dtype, int order) {
-  if (dtype != 0 || order != 1) return 1;
+  if (dtype == 2 || order != 1) return 1;
   return tb3d_max_env() >= 2 ? 2 : 1;
 }
 
@@ -107,9 +107,9 @@ template <class T, class Mask>
 cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
                         int zr_lo, int zr_hi, const T* coef, cudaStream_t s) {
   constexpr int K = 1, M = 3, Q = Lanes<T>::Q, RY = 4, CAP = 27;
-  // 8-warp CTAs for the light star; the heavier masks hold ~160 registers
-  // and run 4-warp CTAs (three resident per SM instead of one).
-  constexpr int SY = std::is_same<Mask, StarMask3<1>>::value ? 4 : 2;
+  // 8-warp CTAs for the fp32 star; fp64 and the heavier masks hold ~160
+  // registers and run 4-warp CTAs (three resident per SM instead of one).
+  constexpr int SY = (std::is_same<Mask, StarMask3<1>>::value && sizeof(T) == 4) ? 4 : 2;
   using G = Tb3Geom<T, Q, K, RY, SY>;
   constexpr int VQ = 16 / sizeof(T);
   if (nx % VQ != 0 || !aligned16(d_in) || !aligned16(d_out)) return cudaErrorNotSupported;
