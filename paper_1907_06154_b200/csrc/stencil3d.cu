@@ -26,7 +26,9 @@ std::vector<T> dense3d_coef(const StencilDesc<T>& st) {
 template <class T, int K> struct Cfg3D;
 template <> struct Cfg3D<float, 0> { static constexpr int RY = 4; };
 template <> struct Cfg3D<float, 1> { static constexpr int RY = 4; };
-template <> struct Cfg3D<float, 2> { static constexpr int RY = 2; };
+// fp32 order 2 (3d13pt, halo-lane kernel): RY = 4 measured +5% at 512^3 and
+// +13% at 2048^2 over RY = 2 (255 registers, no spills).
+template <> struct Cfg3D<float, 2> { static constexpr int RY = 4; };
 template <> struct Cfg3D<double, 0> { static constexpr int RY = 4; };
 template <> struct Cfg3D<double, 1> { static constexpr int RY = 4; };
 template <> struct Cfg3D<double, 2> { static constexpr int RY = 2; };
