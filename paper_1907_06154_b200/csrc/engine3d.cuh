@@ -125,62 +125,107 @@ __device__ __forceinline__ bool colpart3(const T (&pl)[NPL][RY + 2 * K][Q], int 
   return any;
 }
 
-// RY output rows of plane z from the register planes (bidirectional chain).
+// Column partials of filter column j for RG consecutive output rows r0..:
+// taps outer, rows inner, so each weight is fetched once per RG rows (fp64
+// weights are LDC.64 loads, not DFMA operands); per row the tap order -- and
+// so the result -- is exactly colpart3's.
+#ifndef SSAM_3D_RG
+#define SSAM_3D_RG 2  // measured: fp64 27pt / poisson / 7pt +5..6%, fp32 27pt +1.5%; 4 is worse
+#endif
+template <class T, int Q, int K, class Mask, int NROW, int NPL, int RG, int CAP>
+__device__ __forceinline__ bool colpart3_rows(const T (&pl)[NPL][NROW][Q], int ph, int r0, int j,
+                                              const Ssam3DParams<T, CAP>& p, T (&cp)[RG][Q]) {
+  constexpr int M = 2 * K + 1;
+  bool any = false;
+#pragma unroll
+  for (int l = 0; l < M; ++l)
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      if (Mask::has(j, t, l)) {
+        const T c = p.coef[(l * M + j) * M + t];
+        const int s = (ph + l) % NPL;
+#pragma unroll
+        for (int g = 0; g < RG; ++g)
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+            cp[g][q] = any ? fma_t(c, pl[s][r0 + g + t][q], cp[g][q]) : c * pl[s][r0 + g + t][q];
+        any = true;
+      }
+    }
+  return any;
+}
+
+// RY output rows of plane z from the register planes (bidirectional chain),
+// RG rows at a time.
 template <class T, int Q, int K, class Mask, int RY, int NPL, int CAP>
 __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], int ph,
                                              const Ssam3DParams<T, CAP>& p, int z, int y_out0,
                                              int x0, bool owner) {
   constexpr int M = 2 * K + 1;
+  constexpr int NROW = RY + 2 * K;
+  constexpr int RG = (RY % SSAM_3D_RG == 0) ? SSAM_3D_RG : 1;
   const int xlo = p.ring, xhi = p.nx - p.ring;
   const int yhi = p.ny - p.ring;
 #pragma unroll
-  for (int r = 0; r < RY; ++r) {
-    T acc[Q];
+  for (int r0 = 0; r0 < RY; r0 += RG) {
+    T acc[RG][Q];
 #pragma unroll
     for (int j = 0; j <= K; ++j) {
-      T cp[Q];
-      const bool any = colpart3<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, r, j, p, cp);
-      if (j == 0) {
+      T cp[RG][Q];
+      const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, RG, CAP>(pl, ph, r0, j, p, cp);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
-      } else {
-        shift_up1<T, Q>(acc);
-        if (any) {
+      for (int g = 0; g < RG; ++g) {
+        if (j == 0) {
 #pragma unroll
-          for (int q = 0; q < Q; ++q) acc[q] += cp[q];
+          for (int q = 0; q < Q; ++q) acc[g][q] = any ? cp[g][q] : T(0);
+        } else {
+          shift_up1<T, Q>(acc[g]);
+          if (any) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) acc[g][q] += cp[g][q];
+          }
         }
       }
     }
     if constexpr (K > 0) {
-      T accr[Q];
+      T accr[RG][Q];
 #pragma unroll
       for (int j = M - 1; j > K; --j) {
-        T cp[Q];
-        const bool any = colpart3<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, r, j, p, cp);
-        if (j == M - 1) {
+        T cp[RG][Q];
+        const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, RG, CAP>(pl, ph, r0, j, p, cp);
 #pragma unroll
-          for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
-        } else {
-          shift_down1<T, Q>(accr);
-          if (any) {
+        for (int g = 0; g < RG; ++g) {
+          if (j == M - 1) {
 #pragma unroll
-            for (int q = 0; q < Q; ++q) accr[q] += cp[q];
+            for (int q = 0; q < Q; ++q) accr[g][q] = any ? cp[g][q] : T(0);
+          } else {
+            shift_down1<T, Q>(accr[g]);
+            if (any) {
+#pragma unroll
+              for (int q = 0; q < Q; ++q) accr[g][q] += cp[g][q];
+            }
           }
         }
       }
-      shift_down1<T, Q>(accr);
 #pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] += accr[q];
+      for (int g = 0; g < RG; ++g) {
+        shift_down1<T, Q>(accr[g]);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[g][q] += accr[g][q];
+      }
     }
-    const int y = y_out0 + r;
-    if (owner && y < yhi) {
-      T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
-      if (p.vec_ok && x0 >= xlo && x0 + Q <= xhi) {
-        st_q<T, Q>(row, acc);
-      } else {
 #pragma unroll
-        for (int q = 0; q < Q; ++q)
-          if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc[q];
+    for (int g = 0; g < RG; ++g) {
+      const int y = y_out0 + r0 + g;
+      if (owner && y < yhi) {
+        T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
+        if (p.vec_ok && x0 >= xlo && x0 + Q <= xhi) {
+          st_q<T, Q>(row, acc[g]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < Q; ++q)
+            if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc[g][q];
+        }
       }
     }
   }
