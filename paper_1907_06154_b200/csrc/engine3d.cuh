@@ -129,6 +129,9 @@ __device__ __forceinline__ bool colpart3(const T (&pl)[NPL][RY + 2 * K][Q], int 
 // taps outer, rows inner, so each weight is fetched once per RG rows (fp64
 // weights are LDC.64 loads, not DFMA operands); per row the tap order -- and
 // so the result -- is exactly colpart3's.
+#ifndef SSAM_HALO_RG
+#define SSAM_HALO_RG 1
+#endif
 #ifndef SSAM_3D_RG
 #define SSAM_3D_RG 2  // measured: fp64 27pt / poisson / 7pt +5..6%, fp32 27pt +1.5%; 4 is worse
 #endif
@@ -425,6 +428,7 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
   const Ssam3DParams<T, CAP>& p = P.p;
   constexpr int M = 2 * K + 1;
   constexpr int NROW = RY + 2 * K;
+  constexpr int HRG = (RY % SSAM_HALO_RG == 0) ? SSAM_HALO_RG : 1;  // rows per weight fetch
   constexpr int NPL = M;
   constexpr int VQ = 16 / sizeof(T);
   constexpr int BW = 32 * Q + 2 * VQ;  // box width: the strip plus VQ columns each side
@@ -519,10 +523,12 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
       if (z >= z1) break;
       take(z - z0 + 2 * K, pl[(ph + NPL - 1) % NPL], hp[(ph + NPL - 1) % NPL]);
 #pragma unroll
-      for (int r = 0; r < RY; ++r) {
-        // halo chain: inj[m] = h_m(K-1), h_m(c) = h_{m-1}(c-1) + colpart_m(c)
-        T inj[K];
-        {
+      for (int r0 = 0; r0 < RY; r0 += HRG) {
+        // halo chains: inj[g][m] = h_m(K-1), h_m(c) = h_{m-1}(c-1) + colpart_m(c)
+        T inj[HRG][K];
+#pragma unroll
+        for (int g = 0; g < HRG; ++g) {
+          const int r = r0 + g;
           T h[K];
 #pragma unroll
           for (int m = 0; m < K; ++m) {
@@ -550,56 +556,67 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
               else
                 h[c] = any ? h[c - 1] + cp : h[c - 1];
             }
-            inj[m] = h[K - 1];
+            inj[g][m] = h[K - 1];
           }
         }
-        T acc[Q];
+        T acc[HRG][Q];
 #pragma unroll
         for (int j = 0; j <= K; ++j) {
-          T cp[Q];
-          const bool any = colpart3<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, r, j, p, cp);
-          if (j == 0) {
+          T cp[HRG][Q];
+          const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, cp);
 #pragma unroll
-            for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
-          } else {
-            shift_up1<T, Q>(acc);
-            if (lane == 0) acc[0] = inj[j - 1];
-            if (any) {
+          for (int g = 0; g < HRG; ++g) {
+            if (j == 0) {
 #pragma unroll
-              for (int q = 0; q < Q; ++q) acc[q] += cp[q];
+              for (int q = 0; q < Q; ++q) acc[g][q] = any ? cp[g][q] : T(0);
+            } else {
+              shift_up1<T, Q>(acc[g]);
+              if (lane == 0) acc[g][0] = inj[g][j - 1];
+              if (any) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) acc[g][q] += cp[g][q];
+              }
             }
           }
         }
-        T accr[Q];
+        T accr[HRG][Q];
 #pragma unroll
         for (int j = M - 1; j > K; --j) {
-          T cp[Q];
-          const bool any = colpart3<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, r, j, p, cp);
-          if (j == M - 1) {
+          T cp[HRG][Q];
+          const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, cp);
 #pragma unroll
-            for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
-          } else {
-            shift_down1<T, Q>(accr);
-            if (is_r) accr[Q - 1] = inj[M - 2 - j];
-            if (any) {
+          for (int g = 0; g < HRG; ++g) {
+            if (j == M - 1) {
 #pragma unroll
-              for (int q = 0; q < Q; ++q) accr[q] += cp[q];
+              for (int q = 0; q < Q; ++q) accr[g][q] = any ? cp[g][q] : T(0);
+            } else {
+              shift_down1<T, Q>(accr[g]);
+              if (is_r) accr[g][Q - 1] = inj[g][M - 2 - j];
+              if (any) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) accr[g][q] += cp[g][q];
+              }
             }
           }
         }
-        shift_down1<T, Q>(accr);
-        if (is_r) accr[Q - 1] = inj[K - 1];
 #pragma unroll
-        for (int q = 0; q < Q; ++q) acc[q] += accr[q];
-        const int y = y_out0 + r;
-        if (y < yhi) {
-          T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
-          if (vec) {
-            st_q<T, Q>(row, acc);
-          } else {
+        for (int g = 0; g < HRG; ++g) {
+          const int r = r0 + g;
+          T acc1[Q];
+          shift_down1<T, Q>(accr[g]);
+          if (is_r) accr[g][Q - 1] = inj[g][K - 1];
 #pragma unroll
-            for (int q = 0; q < Q; ++q)
-              if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc[q];
+          for (int q = 0; q < Q; ++q) acc1[q] = acc[g][q] + accr[g][q];
+          const int y = y_out0 + r;
+          if (y < yhi) {
+            T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
+            if (vec) {
+              st_q<T, Q>(row, acc1);
+            } else {
+#pragma unroll
+              for (int q = 0; q < Q; ++q)
+                if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc1[q];
+            }
           }
         }
       }
