@@ -69,11 +69,6 @@ template <class T> std::vector<T> draws(size_t n, std::uint64_t seed, bool coeff
   return v;
 }
 
-template <class T> constexpr int dtype_of() {
-  return std::is_same_v<T, float> ? SSAM_DTYPE_F32
-                                  : (std::is_same_v<T, double> ? SSAM_DTYPE_F64 : SSAM_DTYPE_I64);
-}
-
 // ---- deterministic JSON records (keys sorted, %.17g doubles) ----------------------
 struct Json {
   std::map<std::string, std::string> kv;

@@ -6,7 +6,6 @@ reference's CPU SSAM path (tests/golden/golden.json) and, when oracle/_ref is
 present, against live reference runs over random configurations.
 """
 import numpy as np
-import pytest
 
 import cases as C
 from oracle import Oracle

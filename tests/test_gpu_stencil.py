@@ -11,7 +11,7 @@ import pytest
 
 import cases as C
 from oracle import Oracle, max_rel_err
-from windows import sample_windows_2d, stencil2d_window, stencil3d_window
+from windows import sample_windows_2d, stencil2d_window
 
 pytestmark = pytest.mark.gpu
 NP = {"f32": np.float32, "f64": np.float64, "i64": np.int64}

@@ -11,7 +11,6 @@ the window touches the domain edge it IS the true ring and nothing is lost.
 """
 from __future__ import annotations
 
-import numpy as np
 
 
 def _span(c0, c1, margin, n):
