@@ -40,56 +40,40 @@ struct alignas(64) Tb2DParams {
 // One stage's output row from its NR-row window (bidirectional chain, as in
 // engine2d.cuh); window row t <-> dy = t - K.
 // Window row t lives in register slot (rot + t) % NR (rotation by index,
-// `rot` folds to a constant after unrolling).
+// `rot` folds to a constant after unrolling).  Single FMA chain per output:
+// every tap FMAs straight into the shifted partial sum -- the reference
+// simulator's stage order (kernels.hpp:111-159) -- so the 1-tap side columns
+// of a star cost one FFMA, not a column-partial FMUL plus an FADD.
 template <class T, int Q, int K, class Mask, int CAP>
 __device__ __forceinline__ void tb_stage_row(const T (&w)[2 * K + 1][Q], int rot,
                                              const Tb2DParams<T, CAP>& p, T (&acc)[Q]) {
   constexpr int NR = 2 * K + 1;
-  auto colpart = [&](int j, T (&cp)[Q]) -> bool {
-    bool any = false;
+  auto colfma = [&](int j, T (&a)[Q]) {
 #pragma unroll
     for (int t = 0; t < NR; ++t) {
       if (Mask::has(j, t)) {
         const T c = p.coef[j * NR + t];
         const int b = (rot + t) % NR;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) cp[q] = any ? fma_t(c, w[b][q], cp[q]) : c * w[b][q];
-        any = true;
+        for (int q = 0; q < Q; ++q) a[q] = fma_t(c, w[b][q], a[q]);
       }
     }
-    return any;
   };
 #pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = T(0);
+#pragma unroll
   for (int j = 0; j <= K; ++j) {
-    T cp[Q];
-    const bool any = colpart(j, cp);
-    if (j == 0) {
-#pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
-    } else {
-      shift_up1<T, Q>(acc);
-      if (any) {
-#pragma unroll
-        for (int q = 0; q < Q; ++q) acc[q] += cp[q];
-      }
-    }
+    if (j > 0) shift_up1<T, Q>(acc);
+    colfma(j, acc);
   }
   if constexpr (K > 0) {
     T accr[Q];
 #pragma unroll
+    for (int q = 0; q < Q; ++q) accr[q] = T(0);
+#pragma unroll
     for (int j = NR - 1; j > K; --j) {
-      T cp[Q];
-      const bool any = colpart(j, cp);
-      if (j == NR - 1) {
-#pragma unroll
-        for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
-      } else {
-        shift_down1<T, Q>(accr);
-        if (any) {
-#pragma unroll
-          for (int q = 0; q < Q; ++q) accr[q] += cp[q];
-        }
-      }
+      if (j < NR - 1) shift_down1<T, Q>(accr);
+      colfma(j, accr);
     }
     shift_down1<T, Q>(accr);
 #pragma unroll
@@ -114,6 +98,10 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
   const bool own = x0 >= x_out0 && x0 < x_out0 + p.V;
   const int xlo = p.ring, xhi = p.W - p.ring;
   const bool whole = x0 >= xlo && x0 + Q <= xhi;
+  // Does any stage row of this warp fall on the ring (columns of the window,
+  // or rows y0 - TB*K .. y1 + TB*K)?  Warp-uniform.
+  const bool edge = base < xlo || base + 32 * Q > xhi || y0 - TB * K < p.ring ||
+                    y1 + TB * K > p.H - p.ring;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(wib) * D * RB * ROW;
@@ -165,15 +153,19 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
         const int y = r - (st + 1) * K;
         T acc[Q];
         tb_stage_row<T, Q, K, Mask, CAP>(win[st], rr + 1, p, acc);
-        // ring cells keep their (generation-invariant) value
-        const bool row_ring = y < p.ring || y >= p.H - p.ring;
-        const int c = (rr + 1 + K) % NR;  // centre row slot
+        // ring cells keep their (generation-invariant) value; only warps
+        // whose window touches the ring pay for the selects
+        if (edge) {
+          const bool row_ring = y < p.ring || y >= p.H - p.ring;
+          const int c = (rr + 1 + K) % NR;  // centre row slot
 #pragma unroll
-        for (int q = 0; q < Q; ++q) {
-          const int x = x0 + q;
-          if (row_ring || x < xlo || x >= xhi) acc[q] = win[st][c][q];
-          in_row[q] = acc[q];
+          for (int q = 0; q < Q; ++q) {
+            const int x = x0 + q;
+            if (row_ring || x < xlo || x >= xhi) acc[q] = win[st][c][q];
+          }
         }
+#pragma unroll
+        for (int q = 0; q < Q; ++q) in_row[q] = acc[q];
       }
       // in_row now holds generation TB of row r - TB*K
       const int y = r - TB * K;
@@ -288,10 +280,11 @@ template cudaError_t stencil2d_tb<long long>(const long long*, long long*, int, 
 // Deepest fused depth for automatic scheduling (1 = none).
 int stencil2d_tb_max(int dtype, int order, bool star) {
   if (dtype == 2 || !star) return 1;
-  // Measured x100 on 8192^2 (GCells/s, Tb = 1/2/4/8): 2d5pt f32 664/964/1420/1411,
-  // f64 349/595/808/641; 2d9pt f32 661/874/933/-, f64 350/528/476/-.
-  if (order == 1) return 4;  // TB=8 is compiled but no faster (register pressure)
-  if (order == 2) return dtype == 1 ? 2 : 4;
+  // Measured x100 on 8192^2 (GCells/s, Tb = 1/2/4/8; single FMA chain, ring
+  // selects only in edge warps): 2d5pt f32 676/767/1768/1582, f64
+  // 351/441/933/654; 2d9pt f32 675/1166/1009/-, f64 355/590/486/-.
+  if (order == 1) return 4;  // TB=8 is compiled but slower (register pressure)
+  if (order == 2) return 2;
   return 1;
 }
 

@@ -22,6 +22,12 @@ elif kind in ("conv1d", "scan"):
         for _ in range(reps): dev.conv1d(x, y, f)
     else:
         for _ in range(reps): dev.scan(x, y)
+elif kind == "st2dtb":
+    name, dt, tb = sys.argv[2], sys.argv[3], int(sys.argv[4]); H = W = 8192
+    tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)
+    a = torch.empty((H, W), dtype=tdt, device="cuda"); dev.fill_random(a, 0); b = a.clone()
+    st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt)
+    for _ in range(reps): dev.stencil2d_tb(a, b, st, tb)
 elif kind == "st2d":
     name, dt = sys.argv[2], sys.argv[3]; H = W = 8192
     tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)
