@@ -6,6 +6,7 @@
 #pragma once
 
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "engine2d_fma.cuh"
@@ -114,6 +115,14 @@ constexpr bool fma_exact(int k, int q) {
 
 template <class T, int Q, int K>
 cudaError_t conv_fma_sq(const Engine2DArgs<T>& a, cudaStream_t s) {
+  // 7x7 .. 11x11: one FMA chain per output (the reference simulator's stage
+  // order) instead of the paper's two-level column partials: +4..8%
+  // (profiles/r01/conv_chain1_ab.txt), max error 3.1e-6 at 10x10 on 8192^2
+  // (fp32 tolerance 1e-5).  Larger filters keep the two-level order, which
+  // is what holds 17x17 and 20x20 under 1e-5; 6x6 measured
+  // slower with it.
+  if constexpr (K >= 7 && K <= 11 && std::is_same<T, float>::value)
+    return launch_fma2d<T, Q, K, K, fma_ry(K), fma_exact(K, Q), K * K, DenseMask, true>(a, s);
   return launch_fma2d<T, Q, K, K, fma_ry(K), fma_exact(K, Q), K * K>(a, s);
 }
 
