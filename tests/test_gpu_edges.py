@@ -1,0 +1,72 @@
+"""Edge shapes for the newer engines (-m gpu): the FMA conv engine on small /
+odd images, the fused 3D pair on thin grids, conv1d / scan at their size
+limits.  Oracle parity within the reference tolerances (int64 exact)."""
+import numpy as np
+import pytest
+
+from oracle import max_rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = {np.dtype(np.float32): 1e-5, np.dtype(np.float64): 1e-12, np.dtype(np.int64): 0.0}
+
+
+@pytest.mark.parametrize("K", [6, 7, 11, 12, 13, 19, 20])
+@pytest.mark.parametrize("shape", [(20, 32), (41, 64), (97, 132), (256, 260)])
+def test_fma_conv_small_images(cuda_lib, orc, K, shape):
+    h, w = shape
+    if h < K:  # the reference needs H >= n + p - 1
+        pytest.skip("shorter than one cache block")
+    for dt in (np.float32, np.int64):
+        g = orc.random_grid((h, w), dt, K * 7 + h)
+        f = orc.random_filter(K, K, dt, K)
+        cfg = cuda_lib.KernelConfig(p=1)
+        got = cuda_lib.conv2d(g, f, cfg)
+        assert max_rel_err(got, orc.conv2d(g, f, 0)) <= TOL[np.dtype(dt)], (K, shape, dt)
+
+
+@pytest.mark.parametrize("shape", [(3, 3, 8), (4, 5, 16), (5, 3, 132), (7, 40, 260), (33, 17, 68)])
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_tb3d_thin_grids(cuda_lib, orc, shape, dt):
+    import torch
+    from paper_1907_06154_b200 import device as dev
+    st = cuda_lib.convert_stencil(cuda_lib.make_benchmark_stencil("3d7pt"), dt)
+    g = orc.random_grid(shape, dt, 3)
+    a = torch.from_numpy(g).cuda()
+    b, c, f = a.clone(), a.clone(), a.clone()
+    dev.stencil3d_sweep(a, b, st)
+    dev.stencil3d_sweep(b, c, st)
+    dev.stencil3d_tb(a, f, st, 2)
+    assert torch.equal(f, c), shape
+    offs = [t.offset for t in st.taps]
+    cf = np.asarray([t.coeff for t in st.taps], dt)
+    for iters in (1, 2, 5):
+        got = cuda_lib.stencil3d(g, st, cuda_lib.KernelConfig(p=2, b=128), iters)
+        assert max_rel_err(got, orc.stencil3d(g, offs, cf, 1, iters)) <= TOL[np.dtype(dt)]
+
+
+@pytest.mark.parametrize("n", [1, 31, 32, 4095, 4096, 4097, 65537, (1 << 20) + 7])
+def test_scan_sizes_device(cuda_lib, orc, n):
+    import torch
+    from paper_1907_06154_b200 import device as dev
+    v = np.random.default_rng(n).integers(-10**6, 10**6, n).astype(np.int64)
+    x = torch.from_numpy(v).cuda()
+    y = torch.empty_like(x)
+    dev.scan(x, y)
+    assert np.array_equal(y.cpu().numpy(), orc.scan(v))
+    xf = torch.from_numpy(orc.random_grid(n, np.float32, n)).cuda()
+    yf = torch.empty_like(xf)
+    dev.scan(xf, yf)
+    exact = np.cumsum(xf.cpu().numpy().astype(np.longdouble))
+    scale = np.maximum(1.0, np.maximum.accumulate(np.abs(exact))).astype(np.float64)
+    assert float(np.max(np.abs(yf.cpu().numpy().astype(np.longdouble) - exact) / scale)) <= 1e-5
+
+
+@pytest.mark.parametrize("m", [1, 2, 17, 31, 32])
+@pytest.mark.parametrize("n", [32, 33, 127, 4099])
+def test_conv1d_limits(cuda_lib, orc, m, n):
+    for dt in (np.int64, np.float64):
+        sig = orc.random_grid(n, dt, m + n)
+        f = orc.random_filter(m, 1, dt, m).reshape(-1)
+        for bnd in (0, 1):
+            got = cuda_lib.conv1d(sig, f, cuda_lib.KernelConfig(boundary=cuda_lib.Boundary(bnd)))
+            assert max_rel_err(got, orc.conv1d(sig, f, bnd)) <= TOL[np.dtype(dt)], (m, n, bnd)
