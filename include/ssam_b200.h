@@ -185,6 +185,42 @@ int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int
                            const ssam_stencil* st, int tb, void* stream);
 int ssam_b200_stencil3d_tb_max(int dtype, const ssam_stencil* st);
 
+/* Peer-memory halo for z-slab runs (one process per GPU, buffers shared with
+ * CUDA IPC; NVLink P2P across GPUs).  The sweep kernel itself stores the
+ * output planes a neighbour keeps as ghost slots into that neighbour's
+ * buffer, so no separate exchange runs: planes z < lo_end also go to `lo` at
+ * element offset (index + lo_shift), planes z >= hi_begin to `hi` at
+ * (index + hi_shift).  NULL lo / hi: no neighbour on that side.  The caller
+ * orders the sweeps across ranks (neighbours' previous sweep finished before
+ * this one starts, e.g. with IPC events).  Replaces the send/recv pair of the
+ * NCCL path (paper_1907_06154_b200/slab.py); the reference is single-node
+ * single-GPU. */
+typedef struct ssam_peer_halo {
+  void* lo;
+  long long lo_shift;
+  int lo_end;
+  void* hi;
+  long long hi_shift;
+  int hi_begin;
+} ssam_peer_halo;
+
+int ssam_b200_stencil3d_sweep_peer(int dtype, const void* d_in, void* d_out, int nx, int ny,
+                                   int nz, int z_begin, int z_end, const ssam_stencil* st,
+                                   const ssam_peer_halo* peer, void* stream);
+int ssam_b200_stencil3d_tb_peer(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
+                                int z_begin, int z_end, int z_ring_lo, int z_ring_hi,
+                                const ssam_stencil* st, int tb, const ssam_peer_halo* peer,
+                                void* stream);
+
+/* Device buffers shareable across processes (cudaMalloc + CUDA IPC handle of
+ * SSAM_IPC_HANDLE_BYTES bytes).  _open maps a handle exported by another
+ * process (same GPU, or a peer GPU with P2P access); _close unmaps it. */
+#define SSAM_IPC_HANDLE_BYTES 64
+int ssam_b200_ipc_alloc(size_t bytes, void** d_ptr, void* handle);
+int ssam_b200_ipc_free(void* d_ptr);
+int ssam_b200_ipc_open(const void* handle, void** d_ptr);
+int ssam_b200_ipc_close(void* d_ptr);
+
 /* iters sweeps with ping-pong buffers.  d_a holds the input; d_b is scratch
  * of the same size whose ring this call initialises.  *d_result receives
  * d_a or d_b, whichever holds the final generation.  tb: temporal block

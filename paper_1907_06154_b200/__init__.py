@@ -144,6 +144,21 @@ _sig("ssam_b200_sgrd_write", [C.c_char_p, _i, _i, _p, _p, _i, _p])
 _sig("ssam_b200_gather_conv2d", [_i, _p, _i, _i, _p, _i, _i, _i, _p])
 _sig("ssam_b200_gather_stencil", [_i, _p, _i, _i, _i, _PS, _i, _p])
 
+
+class _PeerHalo(C.Structure):
+    _fields_ = [("lo", C.c_void_p), ("lo_shift", C.c_longlong), ("lo_end", C.c_int),
+                ("hi", C.c_void_p), ("hi_shift", C.c_longlong), ("hi_begin", C.c_int)]
+
+
+_PP = C.POINTER(_PeerHalo)
+_sig("ssam_b200_stencil3d_sweep_peer", [_i, _p, _p, _i, _i, _i, _i, _i, _PS, _PP, _p])
+_sig("ssam_b200_stencil3d_tb_peer", [_i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _PS, _i, _PP, _p])
+_sig("ssam_b200_ipc_alloc", [_sz, C.POINTER(_p), _p])
+_sig("ssam_b200_ipc_free", [_p])
+_sig("ssam_b200_ipc_open", [_p, C.POINTER(_p)])
+_sig("ssam_b200_ipc_close", [_p])
+IPC_HANDLE_BYTES = 64
+
 lib = _lib  # raw handle for device-level callers (bench.py, tests)
 
 # Every symbol include/ssam_b200.h declares (checked by tests/test_abi.py).
@@ -161,7 +176,8 @@ EXPORTED = [
     "ssam_b200_counters_scan", "ssam_b200_conv1d_device", "ssam_b200_scan_device",
     "ssam_b200_sgrd_info", "ssam_b200_sgrd_read", "ssam_b200_sgrd_write",
     "ssam_b200_gather_conv2d", "ssam_b200_gather_stencil", "ssam_b200_stencil3d_tb",
-    "ssam_b200_stencil3d_tb_max",
+    "ssam_b200_stencil3d_tb_max", "ssam_b200_stencil3d_sweep_peer", "ssam_b200_stencil3d_tb_peer",
+    "ssam_b200_ipc_alloc", "ssam_b200_ipc_free", "ssam_b200_ipc_open", "ssam_b200_ipc_close",
 ]
 
 

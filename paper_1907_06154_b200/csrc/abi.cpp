@@ -632,7 +632,45 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 namespace ssam_b200 {
 // Status + message for the other host-side units (grid_io.cpp).
 int set_error(int status, const std::string& msg) { return fail(status, msg); }
+
+const PeerHalo*& peer_halo_slot() {
+  thread_local const PeerHalo* h = nullptr;
+  return h;
+}
 }  // namespace ssam_b200
+
+namespace {
+
+PeerHalo to_peer(const ssam_peer_halo* p) {
+  return PeerHalo{p->lo, p->lo_shift, p->lo_end, p->hi, p->hi_shift, p->hi_begin};
+}
+
+// Makes the launches of one ABI call store the peer halo (launch.cuh, apply_peer_halo).
+struct PeerScope {
+  explicit PeerScope(const PeerHalo* h) { peer_halo_slot() = h; }
+  ~PeerScope() { peer_halo_slot() = nullptr; }
+  PeerScope(const PeerScope&) = delete;
+  PeerScope& operator=(const PeerScope&) = delete;
+};
+
+// Copies the written planes [z0, z1) a neighbour mirrors into its buffer
+// (whole planes: ring cells equal on both sides) -- for kernels that do not
+// store the peer halo themselves.
+int push_planes(int dtype, void* d_out, int nx, int ny, int z0, int z1, const PeerHalo& h,
+                cudaStream_t s) {
+  const size_t es = dtype == 0 ? 4 : 8, plane = static_cast<size_t>(nx) * ny * es;
+  char* base = static_cast<char*>(d_out);
+  auto push = [&](void* peer, long long shift, int a, int b) -> cudaError_t {
+    if (!peer || b <= a) return cudaSuccess;
+    char* dst = static_cast<char*>(peer) + (static_cast<long long>(a) * nx * ny + shift) * static_cast<long long>(es);
+    return cudaMemcpyAsync(dst, base + a * plane, (b - a) * plane, cudaMemcpyDefault, s);
+  };
+  cudaError_t e = push(h.lo, h.lo_shift, z0, std::min(z1, h.lo_end));
+  if (e == cudaSuccess) e = push(h.hi, h.hi_shift, std::max(z0, h.hi_begin), z1);
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "stencil3d_sweep_peer: push");
+}
+
+}  // namespace
 
 // ===========================================================================
 extern "C" {
@@ -1057,6 +1095,80 @@ int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int
 int ssam_b200_stencil3d_tb_max(int dtype, const ssam_stencil* st) {
   if (!st || st->dims != 3 || !dtype_ok(dtype)) return 1;
   return stencil3d_tb_max(dtype, st->order);
+}
+
+int ssam_b200_stencil3d_sweep_peer(int dtype, const void* d_in, void* d_out, int nx, int ny,
+                                   int nz, int z_begin, int z_end, const ssam_stencil* st,
+                                   const ssam_peer_halo* peer, void* stream) {
+  if (!peer) return ssam_b200_stencil3d_sweep(dtype, d_in, d_out, nx, ny, nz, z_begin, z_end, st, stream);
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = validate_stencil(st)) return s;
+  const PeerHalo h = to_peer(peer);
+  int rc;
+  {
+    PeerScope scope(&h);
+    rc = ssam_b200_stencil3d_sweep(dtype, d_in, d_out, nx, ny, nz, z_begin, z_end, st, stream);
+  }
+  if (rc != SSAM_OK || stencil3d_peer_fused(dtype, st->order)) return rc;
+  // direct-gather kernel (order > 2): push the boundary planes after it
+  return push_planes(dtype, d_out, nx, ny, std::max(z_begin, st->order),
+                     std::min(z_end, nz - st->order), h, as_stream(stream));
+}
+
+int ssam_b200_stencil3d_tb_peer(int dtype, const void* d_in, void* d_out, int nx, int ny, int nz,
+                                int z_begin, int z_end, int z_ring_lo, int z_ring_hi,
+                                const ssam_stencil* st, int tb, const ssam_peer_halo* peer,
+                                void* stream) {
+  if (!peer)
+    return ssam_b200_stencil3d_tb(dtype, d_in, d_out, nx, ny, nz, z_begin, z_end, z_ring_lo,
+                                  z_ring_hi, st, tb, stream);
+  const PeerHalo h = to_peer(peer);
+  PeerScope scope(&h);
+  return ssam_b200_stencil3d_tb(dtype, d_in, d_out, nx, ny, nz, z_begin, z_end, z_ring_lo,
+                                z_ring_hi, st, tb, stream);
+}
+
+static_assert(sizeof(cudaIpcMemHandle_t) == SSAM_IPC_HANDLE_BYTES, "IPC handle size");
+
+int ssam_b200_ipc_alloc(size_t bytes, void** d_ptr, void* handle) {
+  g_err.clear();
+  if (!d_ptr || !handle || bytes == 0) return fail(SSAM_ERR_INVALID_ARGUMENT, "ipc_alloc: bad argument");
+  if (int s = device_ready()) return s;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "ipc_alloc");
+  cudaIpcMemHandle_t hd;
+  e = cudaIpcGetMemHandle(&hd, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(e, "ipc_alloc: handle");
+  }
+  std::memcpy(handle, &hd, sizeof(hd));
+  *d_ptr = p;
+  return SSAM_OK;
+}
+
+int ssam_b200_ipc_free(void* d_ptr) {
+  g_err.clear();
+  const cudaError_t e = cudaFree(d_ptr);
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "ipc_free");
+}
+
+int ssam_b200_ipc_open(const void* handle, void** d_ptr) {
+  g_err.clear();
+  if (!d_ptr || !handle) return fail(SSAM_ERR_INVALID_ARGUMENT, "ipc_open: bad argument");
+  if (int s = device_ready()) return s;
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  const cudaError_t e = cudaIpcOpenMemHandle(d_ptr, hd, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "ipc_open");
+}
+
+int ssam_b200_ipc_close(void* d_ptr) {
+  g_err.clear();
+  const cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "ipc_close");
 }
 
 }  // extern "C"

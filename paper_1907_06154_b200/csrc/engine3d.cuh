@@ -39,6 +39,13 @@ struct Ssam3DParams {
   int cta_sx;       // TMA kernel: adjacent x-strips per CTA (sharing one box)
   int zfast;        // TMA kernels: grid is (x, z-segment, y-group) instead of (x, y, z)
   int zr_lo, zr_hi; // fused (Tb > 1) kernel: planes outside [zr_lo, zr_hi) are global ring
+  // Peer-memory halo (slab runs, ssam_peer_halo): output planes z < peer_lo_end
+  // are also stored to peer_lo at element offset + peer_lo_shift, planes
+  // z >= peer_hi_begin to peer_hi (the neighbours' ghost slots).
+  T* peer_lo;
+  T* peer_hi;
+  long long peer_lo_shift, peer_hi_shift;
+  int peer_lo_end, peer_hi_begin;
   T coef[CAP];      // coef[(l*M + j)*M + t], l = dz+K, j = dx+K, t = dy+K
 };
 
@@ -64,6 +71,40 @@ struct PoissonMask3 {
     return (j != 1) + (t != 1) + (l != 1) <= 2;
   }
 };
+
+// Stores one lane's Q outputs of row (z, y) at column x0 (vector when `vec`,
+// else only the columns inside [xlo, xhi)), and mirrors planes a neighbour
+// keeps as ghost slots into its buffer over peer memory.
+template <class T, int Q>
+__device__ __forceinline__ void put_q3(T* row, const T (&v)[Q], bool vec, int x0, int xlo, int xhi) {
+  if (vec) {
+    st_q<T, Q>(row, v);
+  } else {
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+      if (x0 + q >= xlo && x0 + q < xhi) row[q] = v[q];
+  }
+}
+// Whether output plane z is mirrored into a neighbour's ghost slots (uniform
+// per plane; false outside peer-halo slab runs).
+template <class P>
+__device__ __forceinline__ bool mirrored3(const P& p, int z) {
+  return (p.peer_lo != nullptr && z < p.peer_lo_end) ||
+         (p.peer_hi != nullptr && z >= p.peer_hi_begin);
+}
+template <class T, int Q, class P>
+__device__ __forceinline__ void store_row3(const P& p, int z, int y, int x0, const T (&v)[Q],
+                                           bool vec, int xlo, int xhi, bool mirror) {
+  T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
+  put_q3<T, Q>(row, v, vec, x0, xlo, xhi);
+  if (mirror) {
+    const long long off = row - p.out;
+    if (p.peer_lo != nullptr && z < p.peer_lo_end)
+      put_q3<T, Q>(p.peer_lo + (off + p.peer_lo_shift), v, vec, x0, xlo, xhi);
+    if (p.peer_hi != nullptr && z >= p.peer_hi_begin)
+      put_q3<T, Q>(p.peer_hi + (off + p.peer_hi_shift), v, vec, x0, xlo, xhi);
+  }
+}
 
 // One ring slot: a brows x bcols box, padded to the 128-byte alignment TMA
 // requires of every destination.
@@ -160,7 +201,7 @@ __device__ __forceinline__ bool colpart3_rows(const T (&pl)[NPL][NROW][Q], int p
 
 // RY output rows of plane z from the register planes (bidirectional chain),
 // RG rows at a time.
-template <class T, int Q, int K, class Mask, int RY, int NPL, int CAP>
+template <class T, int Q, int K, class Mask, int RY, int NPL, int CAP, bool PEER>
 __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], int ph,
                                              const Ssam3DParams<T, CAP>& p, int z, int y_out0,
                                              int x0, bool owner) {
@@ -169,6 +210,7 @@ __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], 
   constexpr int RG = (RY % SSAM_3D_RG == 0) ? SSAM_3D_RG : 1;
   const int xlo = p.ring, xhi = p.nx - p.ring;
   const int yhi = p.ny - p.ring;
+  const bool mirror = PEER && mirrored3(p, z);
 #pragma unroll
   for (int r0 = 0; r0 < RY; r0 += RG) {
     T acc[RG][Q];
@@ -220,16 +262,9 @@ __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], 
 #pragma unroll
     for (int g = 0; g < RG; ++g) {
       const int y = y_out0 + r0 + g;
-      if (owner && y < yhi) {
-        T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
-        if (p.vec_ok && x0 >= xlo && x0 + Q <= xhi) {
-          st_q<T, Q>(row, acc[g]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < Q; ++q)
-            if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc[g][q];
-        }
-      }
+      if (owner && y < yhi)
+        store_row3<T, Q>(p, z, y, x0, acc[g], p.vec_ok && x0 >= xlo && x0 + Q <= xhi, xlo, xhi,
+                         mirror);
     }
   }
 }
@@ -243,7 +278,7 @@ __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], 
 // i-1 -- one plane of slack so it rarely waits on the slowest warp.
 // Out-of-range rows, planes and columns arrive as zeros (interior outputs
 // never read them).
-template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP>
+template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP, bool PEER = false>
 __global__ void __launch_bounds__(256)
     ssam3d_tma_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
   const Ssam3DParams<T, CAP>& p = P.p;
@@ -323,13 +358,13 @@ __global__ void __launch_bounds__(256)
       const int z = zb + ph;
       if (z >= z1) break;
       take(z - z0 + 2 * K, pl[(ph + NPL - 1) % NPL]);
-      compute_rows<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, p, z, y_out0, x0, owner);
+      compute_rows<T, Q, K, Mask, RY, NPL, CAP, PEER>(pl, ph, p, z, y_out0, x0, owner);
     }
   }
 }
 
 // Direct-load kernel (rows not 16-byte aligned).
-template <class T, int Q, int K, class Mask, int RY, int CAP>
+template <class T, int Q, int K, class Mask, int RY, int CAP, bool PEER = false>
 __global__ void __launch_bounds__(128) ssam3d_kernel(const __grid_constant__ Ssam3DParams<T, CAP> p) {
   constexpr int M = 2 * K + 1;
   constexpr int NROW = RY + 2 * K;
@@ -355,7 +390,7 @@ __global__ void __launch_bounds__(128) ssam3d_kernel(const __grid_constant__ Ssa
       if (z >= z1) break;
       load_plane<T, Q, NROW>(p.in, p.nx, p.ny, p.nz, z + K, y_out0 - K, x0,
                              pl[(ph + NPL - 1) % NPL]);
-      compute_rows<T, Q, K, Mask, RY, NPL, CAP>(pl, ph, p, z, y_out0, x0, owner);
+      compute_rows<T, Q, K, Mask, RY, NPL, CAP, PEER>(pl, ph, p, z, y_out0, x0, owner);
     }
   }
 }
@@ -420,7 +455,7 @@ __host__ __device__ constexpr int halo3d_min_blocks() {
   return halo3d_light<T, K, Mask>() ? 2 : (sizeof(T) == 4 && K == 1 ? 3 : 1);
 }
 
-template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP>
+template <class T, int Q, int K, class Mask, int RY, int DZ, int CAP, bool PEER = false>
 __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
                                   (halo3d_min_blocks<T, K, Mask>()))
     ssam3d_halo_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
@@ -522,6 +557,7 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
       const int z = zb + ph;
       if (z >= z1) break;
       take(z - z0 + 2 * K, pl[(ph + NPL - 1) % NPL], hp[(ph + NPL - 1) % NPL]);
+      const bool mirror = PEER && mirrored3(p, z);
 #pragma unroll
       for (int r0 = 0; r0 < RY; r0 += HRG) {
         // halo chains: inj[g][m] = h_m(K-1), h_m(c) = h_{m-1}(c-1) + colpart_m(c)
@@ -608,16 +644,7 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
 #pragma unroll
           for (int q = 0; q < Q; ++q) acc1[q] = acc[g][q] + accr[g][q];
           const int y = y_out0 + r;
-          if (y < yhi) {
-            T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
-            if (vec) {
-              st_q<T, Q>(row, acc1);
-            } else {
-#pragma unroll
-              for (int q = 0; q < Q; ++q)
-                if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc1[q];
-            }
-          }
+          if (y < yhi) store_row3<T, Q>(p, z, y, x0, acc1, vec, xlo, xhi, mirror);
         }
       }
     }

@@ -107,7 +107,7 @@ struct Tb3Geom {
       DZ * IN_SLOT + DI * MID_SLOT + (2 * DZ + 2 * DI) * 8 + THREADS * 4;
 };
 
-template <class T, int Q, int K, class Mask, int RY, int CAP, int SY = 4>
+template <class T, int Q, int K, class Mask, int RY, int CAP, int SY = 4, bool PEER = false>
 __global__ void __launch_bounds__(2 * SY * 32)
     ssam3d_tb2_kernel(const __grid_constant__ Ssam3DTmaParams<T, CAP> P) {
   using G = Tb3Geom<T, Q, K, RY, SY>;
@@ -242,21 +242,13 @@ __global__ void __launch_bounds__(2 * SY * 32)
         const int z = zb + ph;
         if (z >= z1) break;
         take(z - z0 + 2 * K, pl[(ph + NPL - 1) % NPL]);
+        const bool mirror = PEER && mirrored3(p, z);
 #pragma unroll
         for (int r = 0; r < RY; ++r) {
           T acc[Q];
           row_chain<T, Q, K, Mask, NROW2, NPL, CAP>(pl, ph, r, p, acc);
           const int y = y_out0 + r;
-          if (owner && y < yhi) {
-            T* row = p.out + (static_cast<size_t>(z) * p.ny + y) * p.nx + x0;
-            if (vec) {
-              st_q<T, Q>(row, acc);
-            } else {
-#pragma unroll
-              for (int q = 0; q < Q; ++q)
-                if (x0 + q >= xlo && x0 + q < xhi) row[q] = acc[q];
-            }
-          }
+          if (owner && y < yhi) store_row3<T, Q>(p, z, y, x0, acc, vec, xlo, xhi, mirror);
         }
       }
     }

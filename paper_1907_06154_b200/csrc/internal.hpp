@@ -87,7 +87,7 @@ cudaError_t stencil3d_direct(const T* d_in, T* d_out, int nx, int ny, int nz, in
 template <class T>
 cudaError_t conv1d_device(const T* d_in, T* d_out, int len, const T* h_w, int m, int boundary,
                           cudaStream_t s);
-// Inclusive prefix sum of n elements (one pass, decoupled look-back).
+// Inclusive prefix sum of n elements (reduce, carry, scan: fixed order).
 template <class T>
 cudaError_t scan_device(const T* d_in, T* d_out, size_t n, cudaStream_t s);
 
@@ -97,6 +97,22 @@ cudaError_t fill_random(int dtype, void* d, std::size_t count, std::uint64_t see
 // max |a-b| / max(1,|b|) and max |a-b| over count elements, into host doubles.
 cudaError_t max_rel_err(int dtype, const void* d_a, const void* d_b, std::size_t count,
                         double* h_rel, double* h_abs, cudaStream_t s);
+
+// Peer-memory halo of the 3D sweep being launched on this thread (slab runs,
+// ssam_peer_halo in ssam_b200.h): the z-streaming kernels also store output
+// planes z < lo_end to `lo` (+ lo_shift elements) and z >= hi_begin to `hi`.
+struct PeerHalo {
+  void* lo;
+  long long lo_shift;
+  int lo_end;
+  void* hi;
+  long long hi_shift;
+  int hi_begin;
+};
+const PeerHalo*& peer_halo_slot();
+// Whether stencil3d_sweep / stencil3d_tb of this stencil run a kernel that
+// honours the peer halo (the register engines; the direct kernel does not).
+bool stencil3d_peer_fused(int dtype, int order);
 
 // How many launches of our kernels the last host call issued (bench evidence).
 void note_launch();

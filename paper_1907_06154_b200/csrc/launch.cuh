@@ -167,6 +167,19 @@ struct Engine3DArgs {
   int z_begin, z_end;
 };
 
+template <class P>
+inline void apply_peer_halo(P& p) {
+  using T = typename std::remove_pointer<decltype(p.out)>::type;
+  if (const PeerHalo* h = peer_halo_slot()) {
+    p.peer_lo = static_cast<T*>(h->lo);
+    p.peer_lo_shift = h->lo_shift;
+    p.peer_lo_end = h->lo_end;
+    p.peer_hi = static_cast<T*>(h->hi);
+    p.peer_hi_shift = h->hi_shift;
+    p.peer_hi_begin = h->hi_begin;
+  }
+}
+
 constexpr int kRing3D = 4;  // TMA plane slots per CTA ring (3D engine)
 
 // Warps per 3D CTA (each RY rows); SSAM_B200_3D_WPB overrides (4 or 8).
@@ -240,6 +253,7 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   Ssam3DTmaParams<T, CAP> P;
   std::memset(&P, 0, sizeof(P));
   Ssam3DParams<T, CAP>& p = P.p;
+  apply_peer_halo(p);
   p.in = a.in;
   p.out = a.out;
   p.nx = a.nx;
@@ -297,7 +311,8 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
                                    static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx,
                                    32 * Q + 2 * VQ, sy * RYH + 2 * K);
       if (e != cudaSuccess) return e;
-      auto kern = ssam3d_halo_kernel<T, Q, K, Mask, RYH, DZ, CAP>;
+      auto kern = peer_halo_slot() ? ssam3d_halo_kernel<T, Q, K, Mask, RYH, DZ, CAP, true>
+                                   : ssam3d_halo_kernel<T, Q, K, Mask, RYH, DZ, CAP, false>;
       const size_t smem = halo3d_bytes<T, Q, RYH, K, DZ>(sx, sy);
       if (smem > 48 * 1024) {
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -336,7 +351,8 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
                                  static_cast<uint64_t>(a.ny) * a.nz, sizeof(T) * a.nx,
                                  (sx - 1) * lp.V + 32 * Q, sy * RY + 2 * K);
     if (e != cudaSuccess) return e;
-    auto kern = ssam3d_tma_kernel<T, Q, K, Mask, RY, DZ, CAP>;
+    auto kern = peer_halo_slot() ? ssam3d_tma_kernel<T, Q, K, Mask, RY, DZ, CAP, true>
+                                 : ssam3d_tma_kernel<T, Q, K, Mask, RY, DZ, CAP, false>;
     const size_t smem = ring3d_bytes<T, Q, RY, K, DZ>(sx, sy, lp.V);
     if (smem > 48 * 1024) {
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -347,7 +363,9 @@ cudaError_t launch_ssam3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   } else {
     const dim3 grid(p.nstrips, (p.ygroups + kWarpsPerBlock - 1) / kWarpsPerBlock,
                     (zrows + zseg - 1) / zseg);
-    ssam3d_kernel<T, Q, K, Mask, RY, CAP><<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
+    auto kern = peer_halo_slot() ? ssam3d_kernel<T, Q, K, Mask, RY, CAP, true>
+                                 : ssam3d_kernel<T, Q, K, Mask, RY, CAP, false>;
+    kern<<<grid, 32 * kWarpsPerBlock, 0, s>>>(p);
   }
   note_launch();
   return cudaGetLastError();

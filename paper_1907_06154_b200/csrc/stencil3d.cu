@@ -86,6 +86,8 @@ cudaError_t stencil3d_sweep<long long>(const long long* i, long long* o, int nx,
   return stencil3d_dispatch<long long, false>(i, o, nx, ny, nz, zb, ze, st, s);
 }
 
+bool stencil3d_peer_fused(int dtype, int order) { return order <= (dtype == 2 ? 1 : 2); }
+
 // ---- temporal blocking (Tb = 2), engine3d_tb.cuh --------------------------------
 // SSAM_B200_3D_TB=1 disables the fused path (plain sweeps).
 inline int tb3d_max_env() {
@@ -122,6 +124,7 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
   Ssam3DTmaParams<T, CAP> P;
   std::memset(&P, 0, sizeof(P));
   Ssam3DParams<T, CAP>& p = P.p;
+  apply_peer_halo(p);
   p.in = d_in;
   p.out = d_out;
   p.nx = nx;
@@ -153,7 +156,8 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
   cudaError_t e = make_tmap_2d(&P.tmap, d_in, sizeof(T), nx, static_cast<uint64_t>(ny) * nz,
                                sizeof(T) * nx, G::BW, G::BROWS);
   if (e != cudaSuccess) return e;
-  auto kern = ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP, SY>;
+  auto kern = peer_halo_slot() ? ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP, SY, true>
+                                : ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP, SY, false>;
   e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
   if (e != cudaSuccess) return e;
   e = launch_pdl(kern, grid, dim3(G::THREADS), G::SMEM, s, P);

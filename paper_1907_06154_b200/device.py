@@ -11,7 +11,7 @@ from typing import Optional, Tuple
 
 import numpy as np
 
-from . import (_DT, _StencilArgs, _lib, _raise, InvalidArgument, Stencil)
+from . import (_DT, _PeerHalo, _StencilArgs, _lib, _raise, InvalidArgument, Stencil)
 
 _TORCH_DT = None
 
@@ -87,29 +87,39 @@ def stencil2d_run(d_a, d_b, st: Stencil, iters: int, tb: int = 0, stream=None):
 
 
 def stencil3d_sweep(d_in, d_out, st: Stencil, z_begin: int = 0, z_end: Optional[int] = None,
-                    stream=None) -> None:
+                    stream=None, peer: Optional[_PeerHalo] = None) -> None:
+    """One sweep over output planes [z_begin, z_end); `peer` (ssam_peer_halo)
+    also stores the planes neighbours mirror into their buffers."""
     code = _code(d_in)
     nz, ny, nx = d_in.shape
     sa = _StencilArgs(st, _np_dtype(code))
-    _raise(_lib.ssam_b200_stencil3d_sweep(code, d_in.data_ptr(), d_out.data_ptr(), nx, ny, nz,
-                                          z_begin, nz if z_end is None else z_end, sa.ref,
-                                          _s(stream)))
+    ze = nz if z_end is None else z_end
+    if peer is None:
+        _raise(_lib.ssam_b200_stencil3d_sweep(code, d_in.data_ptr(), d_out.data_ptr(), nx, ny, nz,
+                                              z_begin, ze, sa.ref, _s(stream)))
+    else:
+        _raise(_lib.ssam_b200_stencil3d_sweep_peer(code, d_in.data_ptr(), d_out.data_ptr(), nx, ny,
+                                                   nz, z_begin, ze, sa.ref, C.byref(peer),
+                                                   _s(stream)))
 
 
 def stencil3d_tb(d_in, d_out, st: Stencil, tb: int, z_begin: int = 0,
                  z_end: Optional[int] = None, z_ring_lo: Optional[int] = None,
-                 z_ring_hi: Optional[int] = None, stream=None) -> None:
+                 z_ring_hi: Optional[int] = None, stream=None,
+                 peer: Optional[_PeerHalo] = None) -> None:
     """tb fused 3D sweeps (order-1 stencils, tb = 2) writing planes [z_begin, z_end);
     planes outside [z_ring_lo, z_ring_hi) (default: the buffer's own ring) stay fixed."""
     code = _code(d_in)
     nz, ny, nx = d_in.shape
     sa = _StencilArgs(st, _np_dtype(code))
     k = st.order
-    _raise(_lib.ssam_b200_stencil3d_tb(code, d_in.data_ptr(), d_out.data_ptr(), nx, ny, nz,
-                                       z_begin, nz if z_end is None else z_end,
-                                       k if z_ring_lo is None else z_ring_lo,
-                                       nz - k if z_ring_hi is None else z_ring_hi,
-                                       sa.ref, tb, _s(stream)))
+    args = (code, d_in.data_ptr(), d_out.data_ptr(), nx, ny, nz, z_begin,
+            nz if z_end is None else z_end, k if z_ring_lo is None else z_ring_lo,
+            nz - k if z_ring_hi is None else z_ring_hi, sa.ref, tb)
+    if peer is None:
+        _raise(_lib.ssam_b200_stencil3d_tb(*args, _s(stream)))
+    else:
+        _raise(_lib.ssam_b200_stencil3d_tb_peer(*args, C.byref(peer), _s(stream)))
 
 
 def stencil3d_tb_max(st: Stencil, dtype) -> int:

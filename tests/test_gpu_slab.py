@@ -26,3 +26,17 @@ def test_slab_ranks_match_one_gpu(cuda_lib, world):
                         "--master-port", port, "tools/slab_check.py"],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert "SLAB CHECK PASS" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_halo_slabs_match_one_gpu(cuda_lib, world):
+    """Peer-memory halo (peer.PeerSlabRunner): the sweep kernel stores the
+    neighbours' ghost planes itself over CUDA IPC; 2 and 3 ranks share the GPU.
+    fp32/fp64/int64, Tb 1 and 2, the halo-lane, aligned, dense-K2 and direct
+    (order 3, pushed planes) kernels."""
+    port = str(29650 + world)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+                        "--master-port", port, "tools/peer_slab_check.py"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert "PEER SLAB CHECK PASS" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
