@@ -214,6 +214,9 @@ def workload_config(world: int, args):
             "stencil": STENCIL, "nx": NX, "ny": NY, "nz": NZ_PER_GPU * world,
             "nz_per_gpu": NZ_PER_GPU, "iters_per_step": args.iters,
             "temporal_block": max(1, args.tb),
+            "halo": ("kernel stores into neighbours' CUDA IPC buffers (peer.py)"
+                     if args.halo == "peer" and world > 1 else
+                     "boundary planes first, NCCL send/recv overlapped with the interior"),
             "parallelism": f"z-slab x{world}", "seed": 0,
             "l2": "no flush needed: 8 GiB per buffer >> 126 MB L2"}
 
@@ -236,9 +239,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     k = st.order
     tb = max(1, args.tb)
     slab = decompose(NZ_PER_GPU * world, world, rank, k, ghost=k * tb)
-    a = torch.empty((slab.nz_local, NY, NX), dtype=torch.float32, device="cuda")
+    peer = args.halo == "peer" and world > 1
+    if peer:  # the kernels store the halo into the neighbours' IPC-mapped buffers
+        from paper_1907_06154_b200.peer import PeerSlabRunner
+        group = None if backend() == "gloo" else dist.new_group(backend="gloo")
+        prun = PeerSlabRunner(slab, st, NX, NY, torch.float32, group=group, tb=tb)
+        a, b = prun.a, prun.b
+    else:
+        a = torch.empty((slab.nz_local, NY, NX), dtype=torch.float32, device="cuda")
     fill_slab(a, slab, NX, NY, seed=0)
-    b = a.clone()
+    if peer:
+        b.copy_(a)
+    else:
+        b = a.clone()
     comm = torch.cuda.Stream() if world > 1 else None
 
     launch_ms = []
@@ -271,6 +284,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             dev.stencil3d_tb(cur, nxt, st, tb, zb, ze, rlo, rhi)
 
     runner = SlabRunner(slab, sweep, comm_stream=comm, fused=fused if tb > 1 else None, tb=tb)
+    if peer:
+        runner.run = lambda a_, b_, iters: prun.run(iters)
 
     def barrier():
         if world > 1:
@@ -323,6 +338,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     # free the slab before the e2e / per-kernel phases
     del a, b
+    if peer:
+        prun.close()
     torch.cuda.empty_cache()
 
     e2e = None
@@ -539,6 +556,9 @@ def main():
     ap.add_argument("--tb", type=int, default=1,
                     help="temporal block depth of the headline sweeps (1 or 2)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
+                    help="N > 1 halo transport: NCCL send/recv, or the sweep kernel's own "
+                         "stores into the neighbours' buffers (CUDA IPC / NVLink P2P)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
