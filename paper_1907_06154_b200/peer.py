@@ -68,6 +68,16 @@ def _open(handle: bytes) -> int:
     return ptr.value
 
 
+def peer_geometry(slab: Slab, nz_own_below: int, plane: int):
+    """(lo_shift, lo_end, hi_shift, hi_begin) of ssam_peer_halo for this rank:
+    my local planes z < lo_end are rank-1's top ghost planes at element offset
+    + lo_shift (its local index = mine + nz_own of rank-1), planes z >= hi_begin
+    rank+1's bottom ghosts at + hi_shift (its index = mine - my nz_own)."""
+    own_lo = slab.local(slab.z_first)
+    own_hi = own_lo + slab.nz_own
+    return (nz_own_below * plane, own_lo + slab.ghost, -slab.nz_own * plane, own_hi - slab.ghost)
+
+
 class PeerSlabRunner:
     """Jacobi sweeps on one rank's slab, halos stored by the kernel into the
     neighbours' buffers.  `group` must be a host-side (gloo) group; it carries
@@ -86,9 +96,8 @@ class PeerSlabRunner:
                 "events": [bytes(e.ipc_handle()) for e in self.events]}
         allinfo = [None] * slab.world
         dist.all_gather_object(allinfo, info, group=group)
-        plane = nx * ny
-        own_lo = slab.local(slab.z_first)
-        own_hi = own_lo + slab.nz_own
+        below = allinfo[slab.rank - 1]["nz_own"] if slab.rank > 0 else 0
+        lo_shift, lo_end, hi_shift, hi_begin = peer_geometry(slab, below, nx * ny)
         self.opened = []
         self.nb_events = [[], []]
         self.halo = [_PeerHalo(), _PeerHalo()]
@@ -100,9 +109,9 @@ class PeerSlabRunner:
                 self.opened.append(ptr)
                 h = self.halo[j]
                 if side == 0:  # rank-1 mirrors my lowest `ghost` owned planes as its top ghosts
-                    h.lo, h.lo_shift, h.lo_end = ptr, allinfo[nb]["nz_own"] * plane, own_lo + slab.ghost
+                    h.lo, h.lo_shift, h.lo_end = ptr, lo_shift, lo_end
                 else:          # rank+1 mirrors my highest as its bottom ghosts
-                    h.hi, h.hi_shift, h.hi_begin = ptr, -slab.nz_own * plane, own_hi - slab.ghost
+                    h.hi, h.hi_shift, h.hi_begin = ptr, hi_shift, hi_begin
                 self.nb_events[j].append(
                     torch.cuda.Event.from_ipc_handle(dev_idx, allinfo[nb]["events"][j]))
         self._parity = 0
