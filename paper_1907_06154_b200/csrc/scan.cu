@@ -7,14 +7,15 @@
 // (oracle::scan_naive, oracle.hpp:118-127) -- exact for int64, the only type
 // its tests scan.
 //
-// B200 shape: reduce-then-scan over 256 x 8 rows x 16-byte tiles.
+// B200 shape: reduce-then-scan over 32 KiB tiles (256 threads x rows of 4
+// elements per lane).
 //   1. scan_reduce_kernel: one CTA per tile sums it (read n).
 //   2. scan_carry_kernel: one CTA turns the tile sums into exclusive tile
 //      prefixes (32 serial sums per thread, one block ladder per 32 K tiles).
 //   3. scan_tile_kernel: one CTA per tile scans it from its prefix (read n,
 //      write n).
-// Within a tile every warp owns rows of 32 x 16 bytes (coalesced 512-byte
-// loads and stores); per row each lane scans its 16 bytes serially and the
+// Within a tile every warp owns rows of 32 x 4 elements (coalesced 512-byte /
+// 1 KiB loads and stores); per row each lane scans its 4 elements serially and the
 // 32 lane totals run the same Kogge-Stone shfl_up ladder the reference
 // simulates (5 shuffles), warp totals one more ladder.  A single-pass
 // decoupled look-back (measured here at 2.0-2.5 TB/s on B200: the
@@ -34,10 +35,17 @@ namespace {
 constexpr int kScanThreads = 256;
 constexpr int kCarryThreads = 1024;
 
+// Each lane owns VQ = 4 consecutive elements per row (one 16-byte load for
+// fp32, two for 64-bit types), so the 5-step shuffle ladder is paid per 4
+// elements.  64-bit at 2^28: 2 per lane 2917 GB/s, 4 per lane 3921 (fp64) /
+// 3885 (int64), 8 per lane 3799 / 3930.
+#ifndef SSAM_SCAN_VQ64
+#define SSAM_SCAN_VQ64 4
+#endif
 template <class T>
 struct ScanTile {
-  static constexpr int VQ = 16 / sizeof(T);
-  static constexpr int ROWS = 8;  // 16 KiB (fp32) / 32 KiB (64-bit) tiles
+  static constexpr int VQ = sizeof(T) == 4 ? 4 : SSAM_SCAN_VQ64;
+  static constexpr int ROWS = sizeof(T) == 4 ? 8 : 16 / VQ;  // 32 KiB tiles
   static constexpr int TILE = kScanThreads * ROWS * VQ;
 };
 
@@ -90,11 +98,12 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
-// Exclusive prefix of the tile sums: each of the 1024 threads scans 32
-// consecutive sums serially, one block-wide ladder joins the thread totals,
-// and a running carry links chunks of 32 K sums (one chunk up to 2^30 fp32
-// elements).
-constexpr int kCarryItems = 32;
+// Exclusive prefix of the tile sums: each of the 1024 threads scans
+// kCarryItems consecutive sums serially, one block-wide ladder joins the
+// thread totals, and a running carry links chunks of 1024 * kCarryItems sums
+// (16 items for 64-bit types keeps them in registers).
+template <class T>
+constexpr int carry_items() { return sizeof(T) == 4 ? 32 : 16; }
 
 template <class T>
 __global__ void __launch_bounds__(kCarryThreads)
@@ -104,6 +113,7 @@ __global__ void __launch_bounds__(kCarryThreads)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) s_carry = T(0);
   __syncthreads();
+  constexpr int kCarryItems = carry_items<T>();
   for (long long base = 0; base < tiles; base += static_cast<long long>(kCarryThreads) * kCarryItems) {
     const long long i0 = base + static_cast<long long>(threadIdx.x) * kCarryItems;
     T v[kCarryItems];
