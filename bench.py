@@ -284,15 +284,19 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             dev.stencil3d_tb(cur, nxt, st, tb, zb, ze, rlo, rhi)
 
     runner = SlabRunner(slab, sweep, comm_stream=comm, fused=fused if tb > 1 else None, tb=tb)
-    if peer:
-        runner.run = lambda a_, b_, iters: prun.run(iters)
+
+    def run_step():
+        if peer:
+            prun.run(args.iters)
+        else:
+            runner.run(a, b, args.iters)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     for _ in range(args.warmup):
-        runner.run(a, b, args.iters)
+        run_step()
     torch.cuda.synchronize()
     barrier()
 
@@ -306,7 +310,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     timing["on"] = True
     t_start.record()
     for _ in range(args.steps):
-        runner.run(a, b, args.iters)
+        run_step()
     t_end.record()
     torch.cuda.synchronize()
     timing["on"] = False

@@ -159,7 +159,17 @@ class PeerSlabRunner:
             done += self.tb if fused else 1
         return self.bufs[cur].tensor
 
+    def __enter__(self) -> "PeerSlabRunner":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
     def close(self) -> None:
+        """Collective (every rank calls it): unmaps the neighbours' buffers and
+        frees this rank's."""
+        if not self.bufs:
+            return
         torch.cuda.synchronize()
         dist.barrier(group=self.group)  # no neighbour still writes into our buffers
         for ptr in self.opened:
@@ -168,3 +178,4 @@ class PeerSlabRunner:
         dist.barrier(group=self.group)  # every mapping of our buffers is closed
         for b in self.bufs:
             b.free()
+        self.bufs = []
