@@ -19,6 +19,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "engine2d.cuh"
 
@@ -199,6 +201,40 @@ __device__ __forceinline__ bool colpart3_rows(const T (&pl)[NPL][NROW][Q], int p
   return any;
 }
 
+// Single-chain accumulation: the taps of filter column j are FMAs straight
+// into the running chain value -- no separate column partial, so no FMUL to
+// start it and no FADD to join it.  Fewer FP ops, but one long dependent
+// chain instead of independent column partials; measured per shape at 512^3
+// (two-level -> single chain, GCells/s): 3d13pt f32 445 -> 460, poisson f64
+// 275 -> 306, but 3d7pt f64 371 -> 359, 3d13pt f64 221 -> 210, and the fused
+// Tb = 2 3d7pt f32 1047 -> 955.  So only those two shapes take it.  Every 3D
+// kernel of one (type, mask) -- aligned, halo-lane, direct, fused Tb = 2 and
+// the halo lanes' mini-chains -- uses the same order, so they stay
+// bit-identical.
+template <class T, class Mask>
+constexpr bool chain1_3d() {
+  return (sizeof(T) == 8 && std::is_same<Mask, PoissonMask3>::value && !std::is_integral<T>::value) ||
+         (sizeof(T) == 4 && std::is_same<Mask, StarMask3<2>>::value);
+}
+template <class T, int Q, int K, class Mask, int NROW, int NPL, int RG, int CAP>
+__device__ __forceinline__ void colfma3_rows(const T (&pl)[NPL][NROW][Q], int ph, int r0, int j,
+                                             const Ssam3DParams<T, CAP>& p, T (&acc)[RG][Q]) {
+  constexpr int M = 2 * K + 1;
+#pragma unroll
+  for (int l = 0; l < M; ++l)
+#pragma unroll
+    for (int t = 0; t < M; ++t) {
+      if (Mask::has(j, t, l)) {
+        const T c = p.coef[(l * M + j) * M + t];
+        const int s = (ph + l) % NPL;
+#pragma unroll
+        for (int g = 0; g < RG; ++g)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[g][q] = fma_t(c, pl[s][r0 + g + t][q], acc[g][q]);
+      }
+    }
+}
+
 // RY output rows of plane z from the register planes (bidirectional chain),
 // RG rows at a time.
 template <class T, int Q, int K, class Mask, int RY, int NPL, int CAP, bool PEER>
@@ -214,49 +250,85 @@ __device__ __forceinline__ void compute_rows(const T (&pl)[NPL][RY + 2 * K][Q], 
 #pragma unroll
   for (int r0 = 0; r0 < RY; r0 += RG) {
     T acc[RG][Q];
+    if constexpr (chain1_3d<T, Mask>()) {
 #pragma unroll
-    for (int j = 0; j <= K; ++j) {
-      T cp[RG][Q];
-      const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, RG, CAP>(pl, ph, r0, j, p, cp);
+      for (int g = 0; g < RG; ++g)
 #pragma unroll
-      for (int g = 0; g < RG; ++g) {
-        if (j == 0) {
+        for (int q = 0; q < Q; ++q) acc[g][q] = T(0);
 #pragma unroll
-          for (int q = 0; q < Q; ++q) acc[g][q] = any ? cp[g][q] : T(0);
-        } else {
-          shift_up1<T, Q>(acc[g]);
-          if (any) {
+      for (int j = 0; j <= K; ++j) {
+        if (j > 0) {
 #pragma unroll
-            for (int q = 0; q < Q; ++q) acc[g][q] += cp[g][q];
+          for (int g = 0; g < RG; ++g) shift_up1<T, Q>(acc[g]);
+        }
+        colfma3_rows<T, Q, K, Mask, NROW, NPL, RG, CAP>(pl, ph, r0, j, p, acc);
+      }
+      if constexpr (K > 0) {
+        T accr[RG][Q];
+#pragma unroll
+        for (int g = 0; g < RG; ++g)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) accr[g][q] = T(0);
+#pragma unroll
+        for (int j = M - 1; j > K; --j) {
+          if (j < M - 1) {
+#pragma unroll
+            for (int g = 0; g < RG; ++g) shift_down1<T, Q>(accr[g]);
           }
+          colfma3_rows<T, Q, K, Mask, NROW, NPL, RG, CAP>(pl, ph, r0, j, p, accr);
+        }
+#pragma unroll
+        for (int g = 0; g < RG; ++g) {
+          shift_down1<T, Q>(accr[g]);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[g][q] += accr[g][q];
         }
       }
-    }
-    if constexpr (K > 0) {
-      T accr[RG][Q];
+    } else {
 #pragma unroll
-      for (int j = M - 1; j > K; --j) {
+      for (int j = 0; j <= K; ++j) {
         T cp[RG][Q];
         const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, RG, CAP>(pl, ph, r0, j, p, cp);
 #pragma unroll
         for (int g = 0; g < RG; ++g) {
-          if (j == M - 1) {
+          if (j == 0) {
 #pragma unroll
-            for (int q = 0; q < Q; ++q) accr[g][q] = any ? cp[g][q] : T(0);
+            for (int q = 0; q < Q; ++q) acc[g][q] = any ? cp[g][q] : T(0);
           } else {
-            shift_down1<T, Q>(accr[g]);
+            shift_up1<T, Q>(acc[g]);
             if (any) {
 #pragma unroll
-              for (int q = 0; q < Q; ++q) accr[g][q] += cp[g][q];
+              for (int q = 0; q < Q; ++q) acc[g][q] += cp[g][q];
             }
           }
         }
       }
+      if constexpr (K > 0) {
+        T accr[RG][Q];
 #pragma unroll
-      for (int g = 0; g < RG; ++g) {
-        shift_down1<T, Q>(accr[g]);
+        for (int j = M - 1; j > K; --j) {
+          T cp[RG][Q];
+          const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, RG, CAP>(pl, ph, r0, j, p, cp);
 #pragma unroll
-        for (int q = 0; q < Q; ++q) acc[g][q] += accr[g][q];
+          for (int g = 0; g < RG; ++g) {
+            if (j == M - 1) {
+#pragma unroll
+              for (int q = 0; q < Q; ++q) accr[g][q] = any ? cp[g][q] : T(0);
+            } else {
+              shift_down1<T, Q>(accr[g]);
+              if (any) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) accr[g][q] += cp[g][q];
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < RG; ++g) {
+          shift_down1<T, Q>(accr[g]);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[g][q] += accr[g][q];
+        }
       }
     }
 #pragma unroll
@@ -572,65 +644,111 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
             for (int c = K - 1; c >= m; --c) {
               // both sides' colparts with constant-bank weights (lane 31
               // mirrors dx -> -dx); each lane keeps its own side's
-              T cl = T(0), cr = T(0);
-              bool any = false;
+              if constexpr (chain1_3d<T, Mask>()) {
+                T cl = m == 0 ? T(0) : h[c - 1];
+                T cr = cl;
 #pragma unroll
-              for (int l = 0; l < M; ++l)
+                for (int l = 0; l < M; ++l)
 #pragma unroll
-                for (int t = 0; t < M; ++t)
-                  if (Mask::has(m, t, l)) {
-                    const T v = hp[(ph + l) % NPL][r + t][c];
-                    const T wl = p.coef[(l * M + m) * M + t];
-                    const T wr = p.coef[(l * M + (M - 1 - m)) * M + t];
-                    cl = any ? fma_t(wl, v, cl) : wl * v;
-                    cr = any ? fma_t(wr, v, cr) : wr * v;
-                    any = true;
-                  }
-              const T cp = is_r ? cr : cl;
-              if (m == 0)
-                h[c] = any ? cp : T(0);
-              else
-                h[c] = any ? h[c - 1] + cp : h[c - 1];
+                  for (int t = 0; t < M; ++t)
+                    if (Mask::has(m, t, l)) {
+                      const T v = hp[(ph + l) % NPL][r + t][c];
+                      cl = fma_t(p.coef[(l * M + m) * M + t], v, cl);
+                      cr = fma_t(p.coef[(l * M + (M - 1 - m)) * M + t], v, cr);
+                    }
+                h[c] = is_r ? cr : cl;
+              } else {
+                T cl = T(0), cr = T(0);
+                bool any = false;
+#pragma unroll
+                for (int l = 0; l < M; ++l)
+#pragma unroll
+                  for (int t = 0; t < M; ++t)
+                    if (Mask::has(m, t, l)) {
+                      const T v = hp[(ph + l) % NPL][r + t][c];
+                      const T wl = p.coef[(l * M + m) * M + t];
+                      const T wr = p.coef[(l * M + (M - 1 - m)) * M + t];
+                      cl = any ? fma_t(wl, v, cl) : wl * v;
+                      cr = any ? fma_t(wr, v, cr) : wr * v;
+                      any = true;
+                    }
+                const T cp = is_r ? cr : cl;
+                if (m == 0)
+                  h[c] = any ? cp : T(0);
+                else
+                  h[c] = any ? h[c - 1] + cp : h[c - 1];
+              }
             }
             inj[g][m] = h[K - 1];
           }
         }
         T acc[HRG][Q];
+        T accr[HRG][Q];
+        if constexpr (chain1_3d<T, Mask>()) {
 #pragma unroll
-        for (int j = 0; j <= K; ++j) {
-          T cp[HRG][Q];
-          const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, cp);
+          for (int j = 0; j <= K; ++j) {
 #pragma unroll
-          for (int g = 0; g < HRG; ++g) {
-            if (j == 0) {
+            for (int g = 0; g < HRG; ++g) {
+              if (j == 0) {
 #pragma unroll
-              for (int q = 0; q < Q; ++q) acc[g][q] = any ? cp[g][q] : T(0);
-            } else {
-              shift_up1<T, Q>(acc[g]);
-              if (lane == 0) acc[g][0] = inj[g][j - 1];
-              if (any) {
+                for (int q = 0; q < Q; ++q) acc[g][q] = T(0);
+              } else {
+                shift_up1<T, Q>(acc[g]);
+                if (lane == 0) acc[g][0] = inj[g][j - 1];
+              }
+            }
+            colfma3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, acc);
+          }
 #pragma unroll
-                for (int q = 0; q < Q; ++q) acc[g][q] += cp[g][q];
+          for (int j = M - 1; j > K; --j) {
+#pragma unroll
+            for (int g = 0; g < HRG; ++g) {
+              if (j == M - 1) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) accr[g][q] = T(0);
+              } else {
+                shift_down1<T, Q>(accr[g]);
+                if (is_r) accr[g][Q - 1] = inj[g][M - 2 - j];
+              }
+            }
+            colfma3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, accr);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j <= K; ++j) {
+            T cp[HRG][Q];
+            const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, cp);
+#pragma unroll
+            for (int g = 0; g < HRG; ++g) {
+              if (j == 0) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) acc[g][q] = any ? cp[g][q] : T(0);
+              } else {
+                shift_up1<T, Q>(acc[g]);
+                if (lane == 0) acc[g][0] = inj[g][j - 1];
+                if (any) {
+#pragma unroll
+                  for (int q = 0; q < Q; ++q) acc[g][q] += cp[g][q];
+                }
               }
             }
           }
-        }
-        T accr[HRG][Q];
 #pragma unroll
-        for (int j = M - 1; j > K; --j) {
-          T cp[HRG][Q];
-          const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, cp);
+          for (int j = M - 1; j > K; --j) {
+            T cp[HRG][Q];
+            const bool any = colpart3_rows<T, Q, K, Mask, NROW, NPL, HRG, CAP>(pl, ph, r0, j, p, cp);
 #pragma unroll
-          for (int g = 0; g < HRG; ++g) {
-            if (j == M - 1) {
+            for (int g = 0; g < HRG; ++g) {
+              if (j == M - 1) {
 #pragma unroll
-              for (int q = 0; q < Q; ++q) accr[g][q] = any ? cp[g][q] : T(0);
-            } else {
-              shift_down1<T, Q>(accr[g]);
-              if (is_r) accr[g][Q - 1] = inj[g][M - 2 - j];
-              if (any) {
+                for (int q = 0; q < Q; ++q) accr[g][q] = any ? cp[g][q] : T(0);
+              } else {
+                shift_down1<T, Q>(accr[g]);
+                if (is_r) accr[g][Q - 1] = inj[g][M - 2 - j];
+                if (any) {
 #pragma unroll
-                for (int q = 0; q < Q; ++q) accr[g][q] += cp[g][q];
+                  for (int q = 0; q < Q; ++q) accr[g][q] += cp[g][q];
+                }
               }
             }
           }

@@ -37,51 +37,73 @@ template <class T, int Q, int K, class Mask, int NROW, int NPL, int CAP>
 __device__ __forceinline__ void row_chain(const T (&pl)[NPL][NROW][Q], int ph, int r,
                                           const Ssam3DParams<T, CAP>& p, T (&acc)[Q]) {
   constexpr int M = 2 * K + 1;
-  auto colpart = [&](int j, T (&cp)[Q]) {
-    bool any = false;
+  T accr[Q];
+  if constexpr (chain1_3d<T, Mask>()) {
+    // single chain, exactly compute_rows' order (RG = 1)
+    T a2[1][Q], r2[1][Q];
 #pragma unroll
-    for (int l = 0; l < M; ++l)
+    for (int q = 0; q < Q; ++q) a2[0][q] = r2[0][q] = T(0);
 #pragma unroll
-      for (int t = 0; t < M; ++t) {
-        if (Mask::has(j, t, l)) {
-          const T c = p.coef[(l * M + j) * M + t];
-          const int s = (ph + l) % NPL;
+    for (int j = 0; j <= K; ++j) {
+      if (j > 0) shift_up1<T, Q>(a2[0]);
+      colfma3_rows<T, Q, K, Mask, NROW, NPL, 1, CAP>(pl, ph, r, j, p, a2);
+    }
 #pragma unroll
-          for (int q = 0; q < Q; ++q)
-            cp[q] = any ? fma_t(c, pl[s][r + t][q], cp[q]) : c * pl[s][r + t][q];
-          any = true;
+    for (int j = M - 1; j > K; --j) {
+      if (j < M - 1) shift_down1<T, Q>(r2[0]);
+      colfma3_rows<T, Q, K, Mask, NROW, NPL, 1, CAP>(pl, ph, r, j, p, r2);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      acc[q] = a2[0][q];
+      accr[q] = r2[0][q];
+    }
+  } else {
+    auto colpart = [&](int j, T (&cp)[Q]) {
+      bool any = false;
+#pragma unroll
+      for (int l = 0; l < M; ++l)
+#pragma unroll
+        for (int t = 0; t < M; ++t) {
+          if (Mask::has(j, t, l)) {
+            const T c = p.coef[(l * M + j) * M + t];
+            const int s = (ph + l) % NPL;
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+              cp[q] = any ? fma_t(c, pl[s][r + t][q], cp[q]) : c * pl[s][r + t][q];
+            any = true;
+          }
+        }
+      return any;
+    };
+#pragma unroll
+    for (int j = 0; j <= K; ++j) {
+      T cp[Q];
+      const bool any = colpart(j, cp);
+      if (j == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
+      } else {
+        shift_up1<T, Q>(acc);
+        if (any) {
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[q] += cp[q];
         }
       }
-    return any;
-  };
-#pragma unroll
-  for (int j = 0; j <= K; ++j) {
-    T cp[Q];
-    const bool any = colpart(j, cp);
-    if (j == 0) {
-#pragma unroll
-      for (int q = 0; q < Q; ++q) acc[q] = any ? cp[q] : T(0);
-    } else {
-      shift_up1<T, Q>(acc);
-      if (any) {
-#pragma unroll
-        for (int q = 0; q < Q; ++q) acc[q] += cp[q];
-      }
     }
-  }
-  T accr[Q];
 #pragma unroll
-  for (int j = M - 1; j > K; --j) {
-    T cp[Q];
-    const bool any = colpart(j, cp);
-    if (j == M - 1) {
+    for (int j = M - 1; j > K; --j) {
+      T cp[Q];
+      const bool any = colpart(j, cp);
+      if (j == M - 1) {
 #pragma unroll
-      for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
-    } else {
-      shift_down1<T, Q>(accr);
-      if (any) {
+        for (int q = 0; q < Q; ++q) accr[q] = any ? cp[q] : T(0);
+      } else {
+        shift_down1<T, Q>(accr);
+        if (any) {
 #pragma unroll
-        for (int q = 0; q < Q; ++q) accr[q] += cp[q];
+          for (int q = 0; q < Q; ++q) accr[q] += cp[q];
+        }
       }
     }
   }
