@@ -50,7 +50,7 @@ template <class T, int Q, int NR, int MC, int RY, bool EXACT, int CAP, class Mas
           bool CHAIN1 = false>
 cudaError_t launch_fma2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int RB = RY > 4 ? RY : 4;
-  constexpr int D = 3;
+  constexpr int D = fma2d_depth<Mask, CHAIN1, EXACT, MC, NR, RY, RB>();
   if (a.M * NR > CAP || a.NR != NR || (MC > 0 && a.M != MC)) return cudaErrorInvalidValue;
   if (a.y_end <= a.y_begin) return cudaSuccess;
   Ssam2DTmaParams<T, CAP> P;

@@ -60,9 +60,37 @@ __host__ __device__ constexpr size_t fma2d_slot_bytes() {
 
 template <class T, int Q, int NR, int RB, int D, bool EXACT>
 __host__ __device__ constexpr size_t fma2d_smem(int warps, int m) {
-  return static_cast<size_t>(warps) * (D * (fma2d_slot_bytes<T, Q, RB, EXACT>() + 8)) +
+  return 128 +  // guard in front of the ring (STARX reads up to K' columns left of a row)
+         static_cast<size_t>(warps) * (D * (fma2d_slot_bytes<T, Q, RB, EXACT>() + 8)) +
          static_cast<size_t>(warps) * 128 +
          static_cast<size_t>(m) * ((NR * sizeof(T) + 15) / 16 * 16);
+}
+
+// Star footprints (StarMask2D<K>) on the single-chain path take their K
+// horizontal taps on each side straight from the centre row in shared memory
+// (STARX): per output row a lane reads Q + 2K' columns (K' = K rounded up to
+// 16 bytes) with vector LDS instead of running the shuffle chain (one SHFL
+// and Q-1 register moves per column step).  The vertical arm stays in the
+// register window.  The ring then keeps a box until the passes that use its
+// rows as centre rows (K rows behind the window front) are done, so it is
+// deeper (fma2d_depth).  Measured at 8192^2 (chain -> STARX, GCells/s):
+// 2ds25pt (K=6) f32 407 -> 443, f64 236 -> 268; 2d21pt (K=5) f32 477 -> 487,
+// f64 249 -> 270; but 2d17pt (K=4) f32 544 -> 505, f64 319 -> 296 -- so K >= 5.
+template <class Mask> struct StarK2D { static constexpr int value = -1; };
+template <int K> struct StarK2D<StarMask2D<K>> { static constexpr int value = K; };
+#ifndef SSAM_ST2D_STARX
+#define SSAM_ST2D_STARX 1
+#endif
+template <class Mask, bool CHAIN1, bool EXACT, int MC>
+__host__ __device__ constexpr bool fma2d_starx() {
+  return SSAM_ST2D_STARX && CHAIN1 && !EXACT && MC > 0 && StarK2D<Mask>::value >= 5;
+}
+// Ring depth: 3 boxes, or for STARX every box of the prologue and first pass plus one.
+template <class Mask, bool CHAIN1, bool EXACT, int MC, int NR, int RY, int RB>
+__host__ __device__ constexpr int fma2d_depth() {
+  return fma2d_starx<Mask, CHAIN1, EXACT, MC>()
+             ? (fma2d_off(NR, RB) + NR - 1 + RY + RB - 1) / RB + 1
+             : 3;
 }
 
 template <class T, int Q, int NR, int MC, class Mask, int RY, int RB, int D, bool EXACT, int CAP,
@@ -71,6 +99,8 @@ __global__ void __launch_bounds__(128)
     ssam2d_fma_kernel(const __grid_constant__ Ssam2DTmaParams<T, CAP> P) {
   static_assert(RB % RY == 0, "passes never straddle boxes");
   constexpr bool UNROLL = MC > 0;
+  constexpr bool STARX = fma2d_starx<Mask, CHAIN1, EXACT, MC>();
+  constexpr int SK = StarK2D<Mask>::value;
   const Ssam2DParams<T, CAP>& p = P.p;
   constexpr int U = NR - 1 - (NR - 1) / 2;
   constexpr int ROW = fma2d_pitch<EXACT, Q>();  // smem row pitch = box width
@@ -86,7 +116,8 @@ __global__ void __launch_bounds__(128)
   const int nwarps = blockDim.x >> 5;
   const int M = UNROLL ? MC : p.M;
 
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_all[];
+  unsigned char* smem_raw = smem_all + 128;
   T* ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(wib) * D * SLOT;
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(nwarps) * D * SLOT_BYTES) +
@@ -204,7 +235,7 @@ __global__ void __launch_bounds__(128)
     const int s = OFF + t;
     if (t == 0 || s % RB == 0) wait_box(s / RB);
     lds_row(row_ptr(s), win[t]);
-    if ((s + 1) % RB == 0) {  // box s/RB fully read: hand it back once returned
+    if (!STARX && (s + 1) % RB == 0) {  // box s/RB fully read: hand it back once returned
       wait_loaded<T, Q, NW>(win, max(0, t + 1 - RB), min(RB, t + 1), scratch);
       __syncwarp();
       if (lane == 0 && s / RB + D < nbox) issue(s / RB + D);
@@ -214,6 +245,13 @@ __global__ void __launch_bounds__(128)
   T* outp = p.out + static_cast<size_t>(y0) * p.W + x0;
   const size_t W = static_cast<size_t>(p.W);
   int s = OFF + NR - 1;  // first stream row of the pass (a multiple of RY; box-aligned per RB)
+  int rel = 0;           // STARX: next box to hand back
+  // STARX: centre row of the pass's first output row (stream row s - SK) as
+  // (ring slot, row in box); a lane's reads start K' columns left of its own
+  // (lanes reading across a row edge only feed columns the lane plan drops,
+  // and the guard in front of the ring keeps lane 0 of slot 0 in bounds)
+  int cslot = ((s - SK) / RB) % D, cw = (s - SK) % RB;
+  const int hoff = Q * lane - (SK + VQ - 1) / VQ * VQ;
   for (int pass = 0; pass < npass; ++pass, s += RY) {
     if (s % RB == 0) wait_box(s / RB);
     const T* rp = row_ptr(s);
@@ -222,7 +260,44 @@ __global__ void __launch_bounds__(128)
 
     T acc[RY][Q];
     const int R = (M - 1) / 2, L = M - 1 - R;
-    if constexpr (CHAIN1) {
+    if constexpr (STARX) {
+      // vertical arm: filter column SK over the register window
+#pragma unroll
+      for (int r = 0; r < RY; ++r)
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[r][q] = T(0);
+#pragma unroll
+      for (int t = 0; t < NR; ++t) {
+        const T c = p.coef[SK * NR + t];
+#pragma unroll
+        for (int r = 0; r < RY; ++r)
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[r][q] = fma_t(c, win[r + t][q], acc[r][q]);
+      }
+      // horizontal arm: the centre row (stream row s + r - SK) from the ring;
+      // lanes whose reads are clamped at the box edge only feed columns the
+      // lane plan discards
+      constexpr int KP = (SK + VQ - 1) / VQ * VQ, NH = Q + 2 * KP;
+#pragma unroll
+      for (int r = 0; r < RY; ++r) {
+        const bool nxt = cw + r >= RB;  // centre row in the following box
+        const T* rowp = ring + (nxt ? (cslot + 1 == D ? 0 : cslot + 1) : cslot) * SLOT +
+                        (cw + r - (nxt ? RB : 0)) * ROW + hoff;
+        T hx[NH];
+#pragma unroll
+        for (int v = 0; v < NH / VQ; ++v) {
+          const int4 w = *reinterpret_cast<const int4*>(rowp + v * VQ);
+          memcpy(&hx[v * VQ], &w, 16);
+        }
+#pragma unroll
+        for (int j = 0; j < NR; ++j) {
+          if (j == SK) continue;
+          const T c = p.coef[j * NR + SK];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[r][q] = fma_t(c, hx[KP + q + j - SK], acc[r][q]);
+        }
+      }
+    } else if constexpr (CHAIN1) {
       // Single chain (stencils): every tap FMAs straight into the shifted
       // partial sum -- the reference simulator's own stage order (one MAD per
       // tap, a shift between columns, kernels.hpp:111-159) without the
@@ -342,10 +417,24 @@ __global__ void __launch_bounds__(128)
         }
       }
     }
-    // the pass's rows have fed its FFMAs: a box whose last row this was is free
-    if ((s + RY) % RB == 0) {
+    if constexpr (STARX) {
+      // centre rows below s + RY - SK are done: boxes wholly below are free
+      __syncwarp();
+      while ((rel + 1) * RB <= s + RY - SK) {
+        if (lane == 0 && rel + D < nbox) issue(rel + D);
+        ++rel;
+      }
+    } else if ((s + RY) % RB == 0) {
+      // the pass's rows have fed its FFMAs: a box whose last row this was is free
       __syncwarp();
       if (lane == 0 && s / RB + D < nbox) issue(s / RB + D);
+    }
+    if constexpr (STARX) {
+      cw += RY;
+      if (cw >= RB) {
+        cw -= RB;
+        cslot = cslot + 1 == D ? 0 : cslot + 1;
+      }
     }
 #pragma unroll
     for (int t = 0; t < NR - 1; ++t)
