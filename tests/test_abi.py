@@ -68,3 +68,23 @@ def test_catalog_matches_golden(lib, golden):
         assert [float(t.coeff).hex() for t in st.taps] == want["coeffs"]
     with pytest.raises(lib.InvalidArgument):
         lib.make_benchmark_stencil("2d7pt")
+
+
+def test_peer_entry_points_refuse_without_device(lib):
+    """The peer-halo and IPC entry points validate their arguments and fail with
+    a status (never a CPU path) when no GPU is present."""
+    if lib.device_available():
+        pytest.skip("a device is present; covered by the GPU tests")
+    ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(lib.IPC_HANDLE_BYTES)
+    assert lib.lib.ssam_b200_ipc_alloc(0, ctypes.byref(ptr), h) == lib.SSAM_ERR_INVALID_ARGUMENT
+    assert lib.lib.ssam_b200_ipc_alloc(1 << 20, ctypes.byref(ptr), h) != 0
+    assert lib.lib.ssam_b200_ipc_open(None, ctypes.byref(ptr)) == lib.SSAM_ERR_INVALID_ARGUMENT
+    st = lib.convert_stencil(lib.make_benchmark_stencil("3d7pt"), np.float32)
+    sa = lib._StencilArgs(st, np.float32)
+    halo = lib._PeerHalo()
+    rc = lib.lib.ssam_b200_stencil3d_sweep_peer(7, None, None, 8, 8, 8, 0, 8, sa.ref,
+                                                ctypes.byref(halo), None)
+    assert rc == lib.SSAM_ERR_INVALID_ARGUMENT  # unknown dtype, checked first
+    rc = lib.lib.ssam_b200_stencil3d_sweep_peer(0, None, None, 8, 8, 8, 0, 8, sa.ref,
+                                                ctypes.byref(halo), None)
+    assert rc != 0 and lib.lib.ssam_b200_last_error()
