@@ -214,6 +214,9 @@ def workload_config(world: int, args):
             "stencil": STENCIL, "nx": NX, "ny": NY, "nz": NZ_PER_GPU * world,
             "nz_per_gpu": NZ_PER_GPU, "iters_per_step": args.iters,
             "temporal_block": max(1, args.tb),
+            "temporal_blocking": ("each launch fuses temporal_block sweeps (one HBM pass, "
+                                  "bit-identical to single sweeps), as ssam_b200_stencil3d_run "
+                                  "does for this stencil; --tb 1 times single sweeps"),
             "halo": ("kernel stores into neighbours' CUDA IPC buffers (peer.py)"
                      if args.halo == "peer" and world > 1 else
                      "boundary planes first, NCCL send/recv overlapped with the interior"),
@@ -523,6 +526,12 @@ def kernel_suite(peak, sm_mhz):
     dev.fill_random(a, 0)
     bb = a.clone()
     st = ssam.convert_stencil(ssam.make_benchmark_stencil("3d7pt"), np.float32)
+    ms1 = timed(lambda: dev.stencil3d_sweep(a, bb, st), 5)
+    gc1 = (NX - 2) * (NY - 2) * NZ_PER_GPU / ms1 / 1e6
+    out[f"stencil3d_3d7pt_f32_{NX}x{NY}x{NZ_PER_GPU + 2}_tb1"] = {
+        "gcells": round(gc1, 2), "hbm_gbs": round(gc1 * 8, 1),
+        "hbm_frac": round(gc1 * 8 / peak, 4), "ms": round(ms1, 3), "tb": 1,
+        "note": "one sweep per launch (ssam3d_halo_kernel), 8 B/cell"}
     ms = timed(lambda: dev.stencil3d_tb(a, bb, st, 2), 5)
     gc = 2 * (NX - 2) * (NY - 2) * NZ_PER_GPU / ms / 1e6
     out[f"stencil3d_3d7pt_f32_{NX}x{NY}x{NZ_PER_GPU + 2}_tb2"] = {
@@ -557,8 +566,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--iters", type=int, default=100, help="sweeps per step")
-    ap.add_argument("--tb", type=int, default=1,
-                    help="temporal block depth of the headline sweeps (1 or 2)")
+    ap.add_argument("--tb", type=int, default=0,
+                    help="temporal block depth of the headline sweeps: 0 = what the "
+                         "product's ssam_b200_stencil3d_run uses for this stencil (2 for "
+                         "3d7pt f32: fused sweep pairs), 1 = single sweeps")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
                     help="N > 1 halo transport: NCCL send/recv, or the sweep kernel's own "
@@ -569,6 +580,12 @@ def main():
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
+    if args.tb <= 0:  # resolve once so both arms report the same config
+        import numpy as np
+        import paper_1907_06154_b200 as ssam
+        from paper_1907_06154_b200 import device as dev
+        st = ssam.convert_stencil(ssam.make_benchmark_stencil(STENCIL), np.float32)
+        args.tb = dev.stencil3d_tb_max(st, np.float32)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
