@@ -113,7 +113,10 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
   constexpr int K = 1, M = 3, Q = Lanes<T>::Q, RY = 4, CAP = 27;
   // 8-warp CTAs for the fp32 star; fp64 and the heavier masks hold ~160
   // registers and run 4-warp CTAs (three resident per SM instead of one).
-  constexpr int SY = (std::is_same<Mask, StarMask3<1>>::value && sizeof(T) == 4) ? 4 : 2;
+#ifndef SSAM_TB3_SY32
+#define SSAM_TB3_SY32 4
+#endif
+  constexpr int SY = (std::is_same<Mask, StarMask3<1>>::value && sizeof(T) == 4) ? SSAM_TB3_SY32 : 2;
   using G = Tb3Geom<T, Q, K, RY, SY>;
   constexpr int VQ = 16 / sizeof(T);
   if (nx % VQ != 0 || !aligned16(d_in) || !aligned16(d_out)) return cudaErrorNotSupported;
