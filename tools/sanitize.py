@@ -23,7 +23,19 @@ for name in ("3d7pt", "3d13pt", "3d27pt", "poisson"):
     dev.stencil3d_sweep(a3, b3, st)
 st = ssam.convert_stencil(ssam.make_benchmark_stencil("3d7pt"), np.float32)
 dev.stencil3d_tb(a3, b3, st, 2)
+# star arms from shared memory (K >= 5), f32 and f64; 3D single-chain shapes; fp64 fused pair
+for dt, npdt in ((torch.float32, np.float32), (torch.float64, np.float64)):
+    a = grid((70, 132), dt); b = a.clone()
+    for name in ("2d17pt", "2d21pt", "2ds25pt"):
+        dev.stencil2d_sweep(a, b, ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt))
+    a3 = grid((12, 24, 68), dt); b3 = a3.clone()
+    for name in ("3d13pt", "poisson"):
+        dev.stencil3d_sweep(a3, b3, ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt))
+    dev.stencil3d_tb(a3, b3, ssam.convert_stencil(ssam.make_benchmark_stencil("3d7pt"), npdt), 2)
 x = grid(100003); y = torch.empty_like(x)
 dev.conv1d(x, y, np.ones(9, np.float32)); dev.scan(x, y)
+for dt in (torch.float64, torch.int64):
+    x = grid(70001, dt); y = torch.empty_like(x)
+    dev.scan(x, y)
 torch.cuda.synchronize()
 print("sanitize workload done")
