@@ -34,6 +34,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Callable, Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -210,3 +211,44 @@ def fill_slab(t: torch.Tensor, slab: Slab, nx: int, ny: int, seed: int) -> None:
         t[:p0].zero_()
     if p1 < slab.nz_local:
         t[p1:].zero_()
+
+
+# ---------------------------------------------------------------------------
+# 2D: row slabs ("z for 3D, y for 2D").  A (H, W) grid is the
+# nz = H, ny = 1 case of the layout above -- rows are the planes -- so
+# decompose / SlabRunner / fill_slab(t, slab, W, 1, seed) apply unchanged,
+# with device.stencil2d_sweep(cur, nxt, st, y_begin, y_end) as the sweep.
+# conv2d is a single pass over a read-only input: no exchange at all, each
+# rank reads its rows plus the filter's halo rows.
+# ---------------------------------------------------------------------------
+
+def conv2d_halo(n: int) -> int:
+    """Ghost rows a conv2d row slab needs for an n-row filter (anchor
+    ay = (n-1)/2 above, n-1-ay below; oracle.hpp:40-56)."""
+    return n - 1 - (n - 1) // 2
+
+
+def replicate_outside(t: torch.Tensor, slab: Slab) -> None:
+    """Ghost planes beyond the global domain take the nearest edge plane (the
+    replicate boundary, clamp per axis: oracle.hpp:21-28)."""
+    z0 = slab.z_first - slab.ghost
+    p0 = max(0, -z0)
+    p1 = min(slab.nz_local, slab.nz_global - z0)
+    if p0 > 0:
+        t[:p0].copy_(t[p0:p0 + 1].expand_as(t[:p0]))
+    if p1 < slab.nz_local:
+        t[p1:].copy_(t[p1 - 1:p1].expand_as(t[p1:]))
+
+
+def conv2d_slab(d_in: torch.Tensor, d_out: torch.Tensor, weights, slab: Slab,
+                boundary: int = 0, stream=None) -> None:
+    """conv2d of this rank's owned rows.  d_in holds owned rows plus
+    slab.ghost >= conv2d_halo(n) rows each side (fill_slab; zeros beyond the
+    domain for the zero boundary, replicate_outside for replicate); the result
+    lands in d_out's owned rows, equal to the one-GPU conv2d's."""
+    from .device import conv2d
+    n = np.asarray(weights).shape[1]
+    if slab.ghost < conv2d_halo(n):
+        raise ValueError(f"conv2d with {n} filter rows needs ghost >= {conv2d_halo(n)}")
+    own_lo = slab.local(slab.z_first)
+    conv2d(d_in, d_out, weights, boundary, own_lo, own_lo + slab.nz_own, stream=stream)

@@ -40,3 +40,17 @@ def test_peer_halo_slabs_match_one_gpu(cuda_lib, world):
                         "--master-port", port, "tools/peer_slab_check.py"],
                        cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert "PEER SLAB CHECK PASS" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_slabs_2d_match_one_gpu(cuda_lib, world):
+    """2D row slabs (y for 2D): stencil2d sweeps through SlabRunner
+    and conv2d with read-only halo rows (zero and replicate boundaries), f32 /
+    f64 / int64, equal to the one-GPU result bit for bit."""
+    env = dict(os.environ, SSAM_BENCH_BACKEND="gloo")
+    port = str(29700 + world)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        f"--nproc-per-node={world}", "--master-addr", "127.0.0.1",
+                        "--master-port", port, "tools/slab2d_check.py"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert "SLAB2D CHECK PASS" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
