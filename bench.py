@@ -126,6 +126,18 @@ class ClockSampler:
 # reference CPU path (oracle/_ref) -- cpu_baseline and --impl reference
 # ---------------------------------------------------------------------------
 
+def cpu_model() -> str:
+    """Host CPU model (record nproc and the CPU model beside the CPU timing)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def reference_sample(seconds: float = 10.0, max_reps: int = 1000):
     """ssam::stencil3d<float> 3d7pt (the reference's CPU SSAM path, all host
     threads) on a 2048 x 2048 x 16 block of the same seeded grid, repeated
@@ -181,7 +193,8 @@ def run_reference_arm(args, rank: int, world: int):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(world, args),
         "cpu_baseline": {"value": round(value, 6), "unit": "GCells/s",
-                         "cores": ref.max_threads(), "kind": "reference", "sample": sample},
+                         "cores": ref.max_threads(), "kind": "reference", "sample": sample,
+                         "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": round(value, 6), "unit": "GCells/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -365,7 +378,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
         try:
             v, cores, sample = reference_sample(args.cpu_seconds)
             cpu = {"value": round(v, 6), "unit": "GCells/s", "cores": cores, "kind": "reference",
-                   "sample": sample}
+                   "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
         except Exception as ex:  # the reference build may be absent
             cpu = {"value": None, "unit": "GCells/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
