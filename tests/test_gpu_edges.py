@@ -70,3 +70,14 @@ def test_conv1d_limits(cuda_lib, orc, m, n):
         for bnd in (0, 1):
             got = cuda_lib.conv1d(sig, f, cuda_lib.KernelConfig(boundary=cuda_lib.Boundary(bnd)))
             assert max_rel_err(got, orc.conv1d(sig, f, bnd)) <= TOL[np.dtype(dt)], (m, n, bnd)
+
+
+def test_star_arms_random_shapes(cuda_lib):
+    """Random star stencils K = 4..6 (shuffled tap order, random weights) on
+    random shapes, 1-3 sweeps: the FMA engine with the arms read from shared
+    memory (K >= 5) and the chain (K = 4) within tolerance of the oracle."""
+    import subprocess, sys, os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "tools/starx_stress.py", "60"], cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert "STARX STRESS PASS" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
