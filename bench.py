@@ -438,8 +438,12 @@ def e2e_slab(args, slab, st, world, rank):
         comm = torch.cuda.Stream()
         dev_a = torch.empty((nzl, NY, NX), dtype=torch.float32, device="cuda")
         dev_b = torch.empty_like(dev_a)
-        runner = SlabRunner(slab, lambda c, n, zb, ze: dev.stencil3d_sweep(c, n, st, zb, ze),
-                            comm_stream=comm)
+        tb = max(1, args.tb)  # the slab carries k * tb ghost planes (run_ours)
+        rlo, rhi = slab.ring_bounds()
+        runner = SlabRunner(
+            slab, lambda c, n, zb, ze: dev.stencil3d_sweep(c, n, st, zb, ze), comm_stream=comm,
+            fused=(lambda c, n, zb, ze: dev.stencil3d_tb(c, n, st, tb, zb, ze, rlo, rhi))
+            if tb > 1 else None, tb=tb)
 
         def one():
             dev_a.copy_(host_in, non_blocking=True)
@@ -464,7 +468,7 @@ def e2e_slab(args, slab, st, world, rank):
             "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
             "steps": steps, "ms_per_step": round(dt / steps * 1e3, 3),
             "api": "ssam_b200_stencil3d (C ABI, host buffers)" if world == 1 else
-                   "SlabRunner over ssam_b200_stencil3d_sweep (host buffers)"}
+                   "SlabRunner over ssam_b200_stencil3d_sweep / _tb (host buffers)"}
 
 
 def kernel_suite(peak, sm_mhz):
