@@ -167,6 +167,13 @@ int ssam_b200_stencil2d_tb(int dtype, const void* d_in, void* d_out, int width, 
                            const ssam_stencil* st, int tb, void* stream);
 /* Deepest fused temporal block available for (dtype, stencil); 1 = none. */
 int ssam_b200_stencil2d_tb_max(int dtype, const ssam_stencil* st);
+/* stencil2d_tb over output rows [y_begin, y_end) only; rows outside
+ * [y_ring_lo, y_ring_hi) are the global ring and stay fixed (a row slab with
+ * k*tb ghost rows passes its local bounds, which may lie outside the buffer).
+ * Reads rows y_begin-k*tb .. y_end-1+k*tb. */
+int ssam_b200_stencil2d_tb_range(int dtype, const void* d_in, void* d_out, int width, int height,
+                                 int y_begin, int y_end, int y_ring_lo, int y_ring_hi,
+                                 const ssam_stencil* st, int tb, void* stream);
 
 /* One Jacobi sweep over output planes [z_begin, z_end) ∩ [k, nz-k) of an
  * nx x ny x nz buffer (a z-slab with ghost planes passes local indices). */

@@ -121,6 +121,7 @@ _sig("ssam_b200_conv2d_device", [_i, _p, _p, _i, _i, _i, _i, _p, _i, _i, _i, _p]
 _sig("ssam_b200_stencil2d_sweep", [_i, _p, _p, _i, _i, _i, _i, _PS, _p])
 _sig("ssam_b200_stencil2d_tb", [_i, _p, _p, _i, _i, _PS, _i, _p])
 _sig("ssam_b200_stencil2d_tb_max", [_i, _PS])
+_sig("ssam_b200_stencil2d_tb_range", [_i, _p, _p, _i, _i, _i, _i, _i, _i, _PS, _i, _p])
 _sig("ssam_b200_stencil3d_sweep", [_i, _p, _p, _i, _i, _i, _i, _i, _PS, _p])
 _sig("ssam_b200_stencil3d_tb", [_i, _p, _p, _i, _i, _i, _i, _i, _i, _i, _PS, _i, _p])
 _sig("ssam_b200_stencil3d_tb_max", [_i, _PS])
@@ -178,6 +179,7 @@ EXPORTED = [
     "ssam_b200_gather_conv2d", "ssam_b200_gather_stencil", "ssam_b200_stencil3d_tb",
     "ssam_b200_stencil3d_tb_max", "ssam_b200_stencil3d_sweep_peer", "ssam_b200_stencil3d_tb_peer",
     "ssam_b200_ipc_alloc", "ssam_b200_ipc_free", "ssam_b200_ipc_open", "ssam_b200_ipc_close",
+    "ssam_b200_stencil2d_tb_range",
 ]
 
 

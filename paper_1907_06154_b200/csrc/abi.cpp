@@ -882,6 +882,28 @@ int ssam_b200_stencil2d_tb(int dtype, const void* d_in, void* d_out, int w, int 
   return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "stencil2d_tb");
 }
 
+int ssam_b200_stencil2d_tb_range(int dtype, const void* d_in, void* d_out, int w, int h,
+                                 int y_begin, int y_end, int y_ring_lo, int y_ring_hi,
+                                 const ssam_stencil* st, int tb, void* stream) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = validate_stencil(st)) return s;
+  if (st->dims != 2) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil2d: needs a 2D stencil");
+  if (int s = device_ready()) return s;
+  cudaError_t e = cudaErrorInvalidValue;
+  const cudaStream_t s = as_stream(stream);
+  switch (dtype) {
+    case 0: e = stencil2d_tb_range<float>(static_cast<const float*>(d_in), static_cast<float*>(d_out), w, h, y_begin, y_end, y_ring_lo, y_ring_hi, make_desc<float>(st), tb, s); break;
+    case 1: e = stencil2d_tb_range<double>(static_cast<const double*>(d_in), static_cast<double*>(d_out), w, h, y_begin, y_end, y_ring_lo, y_ring_hi, make_desc<double>(st), tb, s); break;
+    case 2: e = stencil2d_tb_range<long long>(static_cast<const long long*>(d_in), static_cast<long long*>(d_out), w, h, y_begin, y_end, y_ring_lo, y_ring_hi, make_desc<long long>(st), tb, s); break;
+  }
+  if (e == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil2d_tb_range: no fused kernel for this case");
+  }
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "stencil2d_tb_range");
+}
+
 int ssam_b200_stencil2d_tb_max(int dtype, const ssam_stencil* st) {
   if (!st || st->dims != 2 || !dtype_ok(dtype)) return 1;
   std::vector<Tap> taps;

@@ -51,6 +51,12 @@ template <class T>
 cudaError_t stencil2d_tb(const T* d_in, T* d_out, int W, int H, const StencilDesc<T>& st, int tb,
                          cudaStream_t s);
 int stencil2d_tb_max(int dtype, int order, bool star);
+// stencil2d_tb over output rows [y_begin, y_end) with the global ring outside
+// rows [yr_lo, yr_hi) (row slabs pass local bounds).
+template <class T>
+cudaError_t stencil2d_tb_range(const T* d_in, T* d_out, int W, int H, int y_begin, int y_end,
+                               int yr_lo, int yr_hi, const StencilDesc<T>& st, int tb,
+                               cudaStream_t s);
 
 // ---- one Jacobi sweep (3D) over output planes [z_begin, z_end) ------------
 // Plane indices are global to the (nz-plane) buffer; the ring test uses

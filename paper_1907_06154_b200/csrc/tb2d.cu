@@ -33,7 +33,9 @@ struct alignas(64) Tb2DParams {
   T* out;
   int W, H;
   int A, V, nstrips, seg, y_begin, y_end;
-  int ring;
+  int ring;          // x ring (k)
+  int yr_lo, yr_hi;  // rows outside [yr_lo, yr_hi) are the global ring (a row slab passes
+                     // its local bounds, which may lie outside the buffer)
   T coef[CAP];
 };
 
@@ -100,8 +102,8 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
   const bool whole = x0 >= xlo && x0 + Q <= xhi;
   // Does any stage row of this warp fall on the ring (columns of the window,
   // or rows y0 - TB*K .. y1 + TB*K)?  Warp-uniform.
-  const bool edge = base < xlo || base + 32 * Q > xhi || y0 - TB * K < p.ring ||
-                    y1 + TB * K > p.H - p.ring;
+  const bool edge = base < xlo || base + 32 * Q > xhi || y0 - TB * K < p.yr_lo ||
+                    y1 + TB * K > p.yr_hi;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   T* ring = reinterpret_cast<T*>(smem_raw) + static_cast<size_t>(wib) * D * RB * ROW;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
         // ring cells keep their (generation-invariant) value; only warps
         // whose window touches the ring pay for the selects
         if (edge) {
-          const bool row_ring = y < p.ring || y >= p.H - p.ring;
+          const bool row_ring = y < p.yr_lo || y >= p.yr_hi;
           const int c = (rr + 1 + K) % NR;  // centre row slot
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
       }
       // in_row now holds generation TB of row r - TB*K
       const int y = r - TB * K;
-      if (own && y >= y0 && y < y1 && y >= p.ring && y < p.H - p.ring) {
+      if (own && y >= y0 && y < y1 && y >= p.yr_lo && y < p.yr_hi) {
         T* row = p.out + static_cast<size_t>(y) * p.W + x0;
         if (whole) {
           st_q<T, Q>(row, in_row);
@@ -197,8 +199,8 @@ std::vector<T> dense_coef(const StencilDesc<T>& st) {
 }
 
 template <class T, int Q, int K, class Mask, int TB>
-cudaError_t launch_tb(const T* in, T* out, int W, int H, const StencilDesc<T>& st,
-                      cudaStream_t s) {
+cudaError_t launch_tb(const T* in, T* out, int W, int H, int yb, int ye, int rlo, int rhi,
+                      const StencilDesc<T>& st, cudaStream_t s) {
   constexpr int NR = 2 * K + 1;
   constexpr int RB = NR;                 // whole-window boxes (rotation by renaming)
   constexpr int D = (12 + RB - 1) / RB;  // ~12 rows in flight per warp
@@ -215,8 +217,10 @@ cudaError_t launch_tb(const T* in, T* out, int W, int H, const StencilDesc<T>& s
   if (p.V <= 0) return cudaErrorNotSupported;
   p.nstrips = (W + lp.V - 1) / lp.V;
   p.ring = K;
-  p.y_begin = K;
-  p.y_end = H - K;
+  p.yr_lo = rlo;
+  p.yr_hi = rhi;
+  p.y_begin = std::max(std::max(yb, rlo), 0);
+  p.y_end = std::min(std::min(ye, rhi), H);
   const int rows = p.y_end - p.y_begin;
   if (rows <= 0 || W - 2 * K <= 0) return cudaSuccess;
   p.seg = std::max(pick_seg(rows, p.nstrips, NR), std::min(rows, 16 * TB * K));
@@ -236,14 +240,15 @@ cudaError_t launch_tb(const T* in, T* out, int W, int H, const StencilDesc<T>& s
 // Fused depths compiled per (dtype, star order); the memory-bound star
 // stencils gain from TB, the compute-heavy ones (k >= 3) do not.
 template <class T, int K>
-cudaError_t tb_dispatch(const T* in, T* out, int W, int H, const StencilDesc<T>& st, int tb,
-                        cudaStream_t s) {
+cudaError_t tb_dispatch(const T* in, T* out, int W, int H, int yb, int ye, int rlo, int rhi,
+                        const StencilDesc<T>& st, int tb, cudaStream_t s) {
   constexpr int Q = 16 / sizeof(T);
   switch (tb) {
-    case 2: return launch_tb<T, Q, K, StarMask2D<K>, 2>(in, out, W, H, st, s);
-    case 4: return launch_tb<T, Q, K, StarMask2D<K>, 4>(in, out, W, H, st, s);
+    case 2: return launch_tb<T, Q, K, StarMask2D<K>, 2>(in, out, W, H, yb, ye, rlo, rhi, st, s);
+    case 4: return launch_tb<T, Q, K, StarMask2D<K>, 4>(in, out, W, H, yb, ye, rlo, rhi, st, s);
     case 8:
-      if constexpr (K == 1) return launch_tb<T, Q, K, StarMask2D<K>, 8>(in, out, W, H, st, s);
+      if constexpr (K == 1)
+        return launch_tb<T, Q, K, StarMask2D<K>, 8>(in, out, W, H, yb, ye, rlo, rhi, st, s);
       return cudaErrorNotSupported;
   }
   return cudaErrorNotSupported;
@@ -252,8 +257,9 @@ cudaError_t tb_dispatch(const T* in, T* out, int W, int H, const StencilDesc<T>&
 }  // namespace
 
 template <class T>
-cudaError_t stencil2d_tb(const T* in, T* out, int W, int H, const StencilDesc<T>& st, int tb,
-                         cudaStream_t s) {
+cudaError_t stencil2d_tb_range(const T* in, T* out, int W, int H, int y_begin, int y_end,
+                               int yr_lo, int yr_hi, const StencilDesc<T>& st, int tb,
+                               cudaStream_t s) {
   if constexpr (std::is_same<T, long long>::value) {
     return cudaErrorNotSupported;
   } else {
@@ -263,15 +269,30 @@ cudaError_t stencil2d_tb(const T* in, T* out, int W, int H, const StencilDesc<T>
       return cudaErrorNotSupported;
     if (classify2d(st.taps, st.order) != Shape2D::star) return cudaErrorNotSupported;
     switch (st.order) {
-      case 1: return tb_dispatch<T, 1>(in, out, W, H, st, tb, s);
-      case 2: return tb_dispatch<T, 2>(in, out, W, H, st, tb, s);
+      case 1: return tb_dispatch<T, 1>(in, out, W, H, y_begin, y_end, yr_lo, yr_hi, st, tb, s);
+      case 2: return tb_dispatch<T, 2>(in, out, W, H, y_begin, y_end, yr_lo, yr_hi, st, tb, s);
     }
     return cudaErrorNotSupported;
   }
 }
 
+template <class T>
+cudaError_t stencil2d_tb(const T* in, T* out, int W, int H, const StencilDesc<T>& st, int tb,
+                         cudaStream_t s) {
+  return stencil2d_tb_range<T>(in, out, W, H, st.order, H - st.order, st.order, H - st.order,
+                               st, tb, s);
+}
+
 template cudaError_t stencil2d_tb<float>(const float*, float*, int, int, const StencilDesc<float>&,
                                          int, cudaStream_t);
+template cudaError_t stencil2d_tb_range<float>(const float*, float*, int, int, int, int, int, int,
+                                               const StencilDesc<float>&, int, cudaStream_t);
+template cudaError_t stencil2d_tb_range<double>(const double*, double*, int, int, int, int, int,
+                                                int, const StencilDesc<double>&, int,
+                                                cudaStream_t);
+template cudaError_t stencil2d_tb_range<long long>(const long long*, long long*, int, int, int,
+                                                   int, int, int, const StencilDesc<long long>&,
+                                                   int, cudaStream_t);
 template cudaError_t stencil2d_tb<double>(const double*, double*, int, int,
                                           const StencilDesc<double>&, int, cudaStream_t);
 template cudaError_t stencil2d_tb<long long>(const long long*, long long*, int, int,

@@ -62,12 +62,23 @@ def stencil2d_sweep(d_in, d_out, st: Stencil, y_begin: int = 0, y_end: Optional[
                                           H if y_end is None else y_end, sa.ref, _s(stream)))
 
 
-def stencil2d_tb(d_in, d_out, st: Stencil, tb: int, stream=None) -> None:
+def stencil2d_tb(d_in, d_out, st: Stencil, tb: int, y_begin: Optional[int] = None,
+                 y_end: Optional[int] = None, y_ring_lo: Optional[int] = None,
+                 y_ring_hi: Optional[int] = None, stream=None) -> None:
+    """tb fused 2D sweeps; with row bounds, only output rows [y_begin, y_end)
+    and rows outside [y_ring_lo, y_ring_hi) kept as the global ring (row slabs)."""
     code = _code(d_in)
     H, W = d_in.shape
     sa = _StencilArgs(st, _np_dtype(code))
-    _raise(_lib.ssam_b200_stencil2d_tb(code, d_in.data_ptr(), d_out.data_ptr(), W, H, sa.ref, tb,
-                                       _s(stream)))
+    if y_begin is None and y_end is None and y_ring_lo is None and y_ring_hi is None:
+        _raise(_lib.ssam_b200_stencil2d_tb(code, d_in.data_ptr(), d_out.data_ptr(), W, H, sa.ref,
+                                           tb, _s(stream)))
+        return
+    k = st.order
+    _raise(_lib.ssam_b200_stencil2d_tb_range(
+        code, d_in.data_ptr(), d_out.data_ptr(), W, H, k if y_begin is None else y_begin,
+        H - k if y_end is None else y_end, k if y_ring_lo is None else y_ring_lo,
+        H - k if y_ring_hi is None else y_ring_hi, sa.ref, tb, _s(stream)))
 
 
 def stencil2d_tb_max(st: Stencil, dtype) -> int:

@@ -48,12 +48,12 @@ def _worker(rank, world, port, kind, arg, q):
         orc = Oracle()
         full = orc.random_grid(SHAPE, np.float64, 5)
         if kind == "stencil":
-            name, iters = arg
+            name, iters, tb = arg
             st = ssam.make_benchmark_stencil(name)
             offs = [t.offset for t in st.taps]
             cf = np.asarray([t.coeff for t in st.taps])
             k = st.order
-            slab = decompose(SHAPE[0], world, rank, k)
+            slab = decompose(SHAPE[0], world, rank, k, ghost=k * tb)
             a = torch.from_numpy(_local_rows(full, slab))
             b = a.clone()
 
@@ -63,7 +63,18 @@ def _worker(rank, world, port, kind, arg, q):
                 out = orc.stencil2d(cur[yb - k:ye + k].numpy(), offs, cf, k, 1)
                 nxt[yb:ye] = torch.from_numpy(out[k:k + (ye - yb)])
 
-            res = SlabRunner(slab, sweep).run(a, b, iters)
+            def fused(cur, nxt, yb, ye):
+                # tb sweeps; sweep j writes [yb - k*(tb-1-j), ye + k*(tb-1-j)) of the global
+                # interior -- what the fused row-range kernel computes on the GPU
+                rlo, rhi = slab.ring_bounds()
+                src = cur
+                for j in range(tb):
+                    w = k * (tb - 1 - j)
+                    dst = nxt if j == tb - 1 else src.clone()
+                    sweep(src, dst, max(yb - w, rlo), min(ye + w, rhi))
+                    src = dst
+
+            res = SlabRunner(slab, sweep, fused=fused if tb > 1 else None, tb=tb).run(a, b, iters)
         else:
             K, bnd = arg
             w = orc.random_filter(K, K, np.float64, K)
@@ -96,16 +107,17 @@ def _run(world, kind, arg):
     return got
 
 
-@pytest.mark.parametrize("world,name", [(2, "2d5pt"), (3, "2d9pt"), (2, "2ds25pt")])
-def test_stencil2d_row_slabs(world, name):
+@pytest.mark.parametrize("world,name,tb", [(2, "2d5pt", 1), (3, "2d9pt", 1), (2, "2ds25pt", 1),
+                                           (2, "2d5pt", 4), (3, "2d9pt", 2)])
+def test_stencil2d_row_slabs(world, name, tb):
     from oracle import Oracle
     import paper_1907_06154_b200 as ssam
     orc = Oracle()
     st = ssam.make_benchmark_stencil(name)
-    iters = 3
+    iters = 2 * tb + 1 if tb > 1 else 3
     want = orc.stencil2d(orc.random_grid(SHAPE, np.float64, 5), [t.offset for t in st.taps],
                          np.asarray([t.coeff for t in st.taps]), st.order, iters)
-    assert np.array_equal(_run(world, "stencil", (name, iters)), want)
+    assert np.array_equal(_run(world, "stencil", (name, iters, tb)), want)
 
 
 @pytest.mark.parametrize("world,K,bnd", [(2, 3, 0), (3, 7, 1), (2, 6, 1), (3, 9, 0)])

@@ -55,6 +55,34 @@ for name, dt, iters in (("2d5pt", np.float32, 5), ("2d9pt", np.float64, 4),
             cur, nxt = nxt, cur
         report(f"stencil2d {name} {np.dtype(dt).name} x{iters}", parts, cur.cpu().numpy())
 
+# fused 2D sweeps on row slabs (ghost = k*Tb, exchange once per Tb sweeps): vs the one-GPU
+# sequence of whole-grid fused launches plus the single-sweep remainder
+for name, dt in (("2d5pt", np.float32), ("2d9pt", np.float32), ("2d5pt", np.float64)):
+    st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), dt)
+    tb = dev.stencil2d_tb_max(st, dt)
+    iters = 2 * tb + 1
+    slab = decompose(H, world, rank, st.order, ghost=st.order * tb)
+    a = torch.empty((slab.nz_local, W), dtype=TD[dt], device="cuda")
+    fill_slab(a, slab, W, 1, seed=9)
+    b = a.clone()
+    rlo, rhi = slab.ring_bounds()
+    runner = SlabRunner(slab, lambda c, n, yb, ye: dev.stencil2d_sweep(c, n, st, yb, ye),
+                        comm_stream=torch.cuda.Stream(),
+                        fused=lambda c, n, yb, ye: dev.stencil2d_tb(c, n, st, tb, yb, ye, rlo, rhi),
+                        tb=tb)
+    parts = gather_rows(slab, runner.run(a, b, iters))
+    if rank == 0:
+        cur = torch.empty((H, W), dtype=TD[dt], device="cuda")
+        dev.fill_random(cur, 9)
+        nxt = cur.clone()
+        for j in range(iters // tb):
+            dev.stencil2d_tb(cur, nxt, st, tb)
+            cur, nxt = nxt, cur
+        for j in range(iters % tb):
+            dev.stencil2d_sweep(cur, nxt, st)
+            cur, nxt = nxt, cur
+        report(f"stencil2d {name} {np.dtype(dt).name} Tb={tb} x{iters}", parts, cur.cpu().numpy())
+
 for K, bnd, dt in ((3, 0, np.float32), (7, 1, np.float32), (20, 0, np.float32),
                    (5, 1, np.float64), (4, 0, np.int64)):
     w = np.random.default_rng(K).uniform(-1, 1, (K, K)).astype(dt) if dt != np.int64 else \
