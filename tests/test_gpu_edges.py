@@ -81,3 +81,14 @@ def test_star_arms_random_shapes(cuda_lib):
     p = subprocess.run([sys.executable, "tools/starx_stress.py", "60"], cwd=root,
                        capture_output=True, text=True, timeout=600)
     assert "STARX STRESS PASS" in p.stdout, p.stdout[-2000:] + p.stderr[-2000:]
+
+
+def test_public_api_fuzz(cuda_lib):
+    """15 s of randomised public-API cases (conv2d any m x n with both
+    boundaries, stencil2d/3d with random tap sets and catalog stencils,
+    conv1d, scan; f32/f64/int64) against the oracle (tools/fuzz.py)."""
+    import subprocess, sys, os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "tools/fuzz.py", "15"], cwd=root, capture_output=True,
+                       text=True, timeout=600, env=dict(os.environ, FUZZ_SEED="11"))
+    assert "FUZZ PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-2000:]
