@@ -110,7 +110,9 @@ int stencil3d_tb_max(int dtype, int order) {
 template <class T, class Mask>
 cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
                         int zr_lo, int zr_hi, const T* coef, cudaStream_t s) {
-  constexpr int K = 1, M = 3, Q = Lanes<T>::Q, RY = 4, CAP = 27;
+  // stage-2 rows per warp: fp32 4 (RY 3 / 5: 937 / 944 vs 1040 GCells/s at
+  // 2048^2 x 514), fp64 5 (504 vs 461 at 2048^2 x 130, 422 vs 388 at 512^3)
+  constexpr int K = 1, M = 3, Q = Lanes<T>::Q, RY = sizeof(T) == 4 ? 4 : 5, CAP = 27;
   // 8-warp CTAs for the fp32 star; fp64 and the heavier masks hold ~160
   // registers and run 4-warp CTAs (three resident per SM instead of one).
 #ifndef SSAM_TB3_SY32
