@@ -74,6 +74,18 @@ cudaError_t stencil3d_tb(const T* d_in, T* d_out, int nx, int ny, int nz, int z_
                          int zr_lo, int zr_hi, const StencilDesc<T>& st, int tb, cudaStream_t s);
 int stencil3d_tb_max(int dtype, int order);
 
+// ---- the order-1 3D star pipeline (star3d.cu, engine3d_star.cuh) ------------
+// coef27: host, the dense 3x3x3 layout coef[(l*3 + j)*3 + t] (l = dz+1,
+// j = dx+1, t = dy+1) with only the 7 star cells used.  star3d_tb fuses tb in
+// {2, 3, 4} sweeps; cudaErrorNotSupported for unaligned grids.
+bool star3d_enabled();
+template <class T>
+cudaError_t star3d_sweep(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
+                         const T* coef27, cudaStream_t s);
+template <class T>
+cudaError_t star3d_tb(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
+                      int zr_lo, int zr_hi, const T* coef27, int tb, cudaStream_t s);
+
 // ---- direct-gather kernels (generic path: any order / tap set) -------------
 // Bit-faithful to the oracle's summation order (double accumulation for FP,
 // no FMA contraction), used where no SSAM specialisation applies.

@@ -54,6 +54,8 @@ cudaError_t stencil3d_dispatch(const T* d_in, T* d_out, int nx, int ny, int nz, 
   Engine3DArgs<T> a{d_in, d_out, nx, ny, nz, k, coef.data(), z_begin, z_end};
   if constexpr (SHAPES) {
     const Shape3D sh = classify3d(st.taps, k);
+    if (k == 1 && sh == Shape3D::star && star3d_enabled())
+      return star3d_sweep<T>(d_in, d_out, nx, ny, nz, z_begin, z_end, coef.data(), s);
     if (k == 1 && sh == Shape3D::star) return st3d<T, 1, StarMask3<1>>(a, s);
     if (k == 2 && sh == Shape3D::star) return st3d<T, 2, StarMask3<2>>(a, s);
     if (k == 1 && sh == Shape3D::poisson) return st3d<T, 1, PoissonMask3>(a, s);
@@ -104,7 +106,9 @@ inline int tb3d_max_env() {
 // 3d27pt -20..30%), so only the 7-point star fuses (run3d checks the shape).
 int stencil3d_tb_max(int dtype, int order) {
   if (dtype == 2 || order != 1) return 1;
-  return tb3d_max_env() >= 2 ? 2 : 1;
+  const int t = tb3d_max_env();
+  if (!star3d_enabled()) return t >= 2 ? 2 : 1;
+  return std::max(1, std::min(t, 4));
 }
 
 template <class T, class Mask>
@@ -124,7 +128,9 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
   if (nx % VQ != 0 || !aligned16(d_in) || !aligned16(d_out)) return cudaErrorNotSupported;
   // outputs [z_begin, z_end) within the global interior [zr_lo, zr_hi); the
   // fused pair reads planes z_begin-2K .. z_end-1+2K (a slab's ghosts)
-  const int zb = std::max(z_begin, zr_lo), ze = std::min(z_end, zr_hi), yrows = ny - 2 * K;
+  // (also clamped to the buffer's interior: ring bounds may lie outside it)
+  const int zb = std::max({z_begin, zr_lo, K}), ze = std::min({z_end, zr_hi, nz - K});
+  const int yrows = ny - 2 * K;
   if (ze <= zb || yrows <= 0 || nx - 2 * K <= 0) return cudaSuccess;
   Ssam3DTmaParams<T, CAP> P;
   std::memset(&P, 0, sizeof(P));
@@ -174,9 +180,13 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
 template <class T>
 cudaError_t stencil3d_tb_impl(const T* d_in, T* d_out, int nx, int ny, int nz, int zb, int ze,
                               int rlo, int rhi, const StencilDesc<T>& st, int tb, cudaStream_t s) {
-  if (tb != 2 || st.order != 1 || std::is_same<T, long long>::value) return cudaErrorNotSupported;
+  if (tb < 2 || st.order != 1 || std::is_same<T, long long>::value) return cudaErrorNotSupported;
   const std::vector<T> coef = dense3d_coef(st);
-  switch (classify3d(st.taps, 1)) {
+  const Shape3D sh = classify3d(st.taps, 1);
+  if (sh == Shape3D::star && star3d_enabled())
+    return star3d_tb<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s);
+  if (tb != 2) return cudaErrorNotSupported;
+  switch (sh) {
     case Shape3D::star:
       return launch_tb3d<T, StarMask3<1>>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), s);
     case Shape3D::poisson:
