@@ -53,6 +53,16 @@ $(VDIR)/%.o: $(SRC)/%.cu $(HDRS)
 $(VDIR)/libssam_b200.so: $(V_OBJS) $(CPP_OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -Xlinker -soname=libssam_b200.so $^ -o $@
 variant: $(VDIR)/libssam_b200.so
+# Quick A/B of one translation unit: recompile only $(VSRC) with VFLAGS and
+# link it with the main build's other objects -> build/qv_$(VAR)/libssam_b200.so
+VSRC ?= star3d
+QDIR := build/qv_$(VAR)
+$(QDIR)/libssam_b200.so: $(SRC)/$(VSRC).cu $(HDRS) $(CU_OBJS) $(CPP_OBJS)
+	@mkdir -p $(QDIR)
+	$(NVCC) $(NVFLAGS) $(VFLAGS) -c $(SRC)/$(VSRC).cu -o $(QDIR)/$(VSRC).o
+	$(NVCC) $(ARCH) -shared -cudart static -Xlinker -soname=libssam_b200.so $(QDIR)/$(VSRC).o $(filter-out $(BUILD)/$(VSRC).o,$(CU_OBJS)) $(CPP_OBJS) -o $@
+qvariant: $(QDIR)/libssam_b200.so
+.PHONY: qvariant
 debug:
 	$(MAKE) variant VAR=dbg VFLAGS=-DSSAM_DEBUG_HANG
 .PHONY: variant debug

@@ -11,16 +11,22 @@ each GPU always owns 2048 x 2048 x 512 cells.
   value   whole-job cell-updates per second (GCells/s), device-resident
           inputs, CUDA events on the compute stream, max over ranks.
   e2e     the same metric through the public C ABI with HOST buffers
-          (ssam_b200_stencil3d at N=1; the slab runner at N>1): pinned
-          host->device copy of the step's input, the sweeps, and the
-          device->host copy of the result inside the timed region.
-  roofline  the dominant kernel (ssam3d_kernel, 3d7pt fp32): algorithmic
-          bytes (4 B read + 4 B write per updated cell) / mean launch time.
+          (ssam_b200_stencil_batch on the 512-plane grid at N=1, bit-compared
+          with the device-resident result; the slab runner at N>1): pinned
+          host->device copy of each step's input, the sweeps, and the
+          device->host copy of its result inside the timed region.
+  roofline  the dominant kernel (star3d_kernel, TB fused sweeps per launch):
+          algorithmic bytes (4 B read + 4 B write per interior cell per
+          launch) / mean launch time; traffic from ncu on this build.
+  parity  every cell of one step (100 sweeps) at N=1 against the
+          direct-gather kernels (the oracle's arithmetic on the GPU):
+          max_rel / max_abs.
   kernels per-kernel GCells/s and %-of-peak for the other configs (conv
           sweep 3x3..20x20, 2D stencils x100 sweeps, 3D stencils at 512^3),
           rank 0 at N=1.
-  cpu_baseline  the reference's own CPU path (oracle/_ref, ssam::stencil3d,
-          all host threads) on a bounded sample of the same workload.
+  cpu_baseline  the reference's own CPU path (oracle/_ref, ssam::stencil3d)
+          on bounded samples of the same workload: threads=0 and threads=1,
+          best of 3 each.
 
 --impl reference times that reference CPU path alone (rank 0; other ranks
 exit 0).  Data are synthetic: the reference's SplitMix64 stream generated on
@@ -54,15 +60,6 @@ def load_peaks():
         return float(p["hbm_gbs"]), "measured", float(p.get("sm_max_mhz", 1965.0))
     except Exception:
         return 6650.0, "fallback", 1965.0
-
-
-def load_traffic():
-    path = os.path.join(ROOT, "profiles", "traffic.json")
-    try:
-        with open(path) as fh:
-            return json.load(fh)
-    except Exception:
-        return {}
 
 
 class ClockSampler:
@@ -138,54 +135,71 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def reference_sample(seconds: float = 10.0, max_reps: int = 1000):
-    """ssam::stencil3d<float> 3d7pt (the reference's CPU SSAM path, all host
-    threads) on a 2048 x 2048 x 16 block of the same seeded grid, repeated
-    single sweeps until `seconds` of CPU work.  Returns (GCells/s, cores, sample)."""
+CPU_BLOCK_NZ = 16     # planes of the threads=0 sample block (14 of them updated per sweep)
+CPU_BLOCK1_NZ = 4     # planes of the threads=1 sample block (2 updated)
+
+
+def _ref_block(nz: int):
+    """A 2048 x 2048 x nz block of the workload's seeded grid (global planes
+    0..nz-1) and the reference's own 3d7pt stencil, for the CPU path."""
     import numpy as np
     from oracle import Oracle, Reference
     ref = Reference()
-    orc = Oracle()
     st = ref.benchmark_stencil(STENCIL)
-    nz = 16
-    g = orc.random_grid((nz, NY, NX), np.float32, 0)
-    cf = st["coeffs"].astype(np.float32)
-    cells = 0
+    g = Oracle().random_grid((nz, NY, NX), np.float32, 0)
+    return ref, st, g, st["coeffs"].astype(np.float32)
+
+
+def _ref_sweep_seconds(ref, st, g, cf, threads: int) -> float:
     t0 = time.perf_counter()
-    reps = 0
-    while reps < max_reps:
-        rc, _, _ = ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128)
-        assert rc == 0
-        cells += g.size
-        reps += 1
-        if time.perf_counter() - t0 >= seconds:
-            break
-    dt = time.perf_counter() - t0
-    return cells / dt / 1e9, ref.max_threads(), \
-        f"{reps} sweep(s) of 3d7pt f32 on a {NX}x{NY}x{nz} block (seed 0), ssam::stencil3d threads=0"
+    rc, _, _ = ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128, threads=threads)
+    assert rc == 0
+    return time.perf_counter() - t0
+
+
+def reference_sample(seconds: float = 10.0):
+    """The reference's own CPU SSAM path (ssam::stencil3d from oracle/_ref,
+    -O3 -fopenmp) on bounded samples of the workload, best of 3 as
+    proj/tools/threads_bench.cpp:25-35 times it: threads=0 (every host
+    thread) on a 2048x2048x16 block and threads=1 on a 2048x2048x4 block.
+    The rate counts the cells of the planes a sweep advances (nz - 2 planes
+    of 2048 x 2048), the same W*H-per-plane convention as the GPU value."""
+    ref, st, g, cf = _ref_block(CPU_BLOCK_NZ)
+    upd = (CPU_BLOCK_NZ - 2) * NX * NY
+    best = min(_ref_sweep_seconds(ref, st, g, cf, 0) for _ in range(3))
+    ref1, st1, g1, cf1 = _ref_block(CPU_BLOCK1_NZ)
+    upd1 = (CPU_BLOCK1_NZ - 2) * NX * NY
+    best1 = min(_ref_sweep_seconds(ref1, st1, g1, cf1, 1) for _ in range(3))
+    return {
+        "value": round(upd / best / 1e9, 6), "unit": "GCells/s", "cores": ref.max_threads(),
+        "kind": "reference",
+        "sample": (f"best of 3 single sweeps of ssam::stencil3d<float> 3d7pt (oracle/_ref, "
+                   f"threads=0 = {ref.max_threads()} threads) on global planes 0..{CPU_BLOCK_NZ - 1} "
+                   f"of the seed-0 grid ({NX}x{NY}x{CPU_BLOCK_NZ}; {CPU_BLOCK_NZ - 2} planes "
+                   f"updated per sweep, counted as {CPU_BLOCK_NZ - 2}*{NX}*{NY} cells)"),
+        "threads1": {"value": round(upd1 / best1 / 1e9, 6), "unit": "GCells/s", "cores": 1,
+                     "sample": (f"best of 3 single sweeps, threads=1, {NX}x{NY}x{CPU_BLOCK1_NZ} "
+                                f"block ({CPU_BLOCK1_NZ - 2} planes updated)")},
+        "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
 
 def run_reference_arm(args, rank: int, world: int):
+    """--impl reference: the reference's own CPU path only (oracle/_ref via
+    oracle/__init__.py); the product library is never loaded here."""
     if rank != 0:
         return
-    import numpy as np
-    from oracle import Oracle, Reference
-    ref = Reference()
-    orc = Oracle()
-    st = ref.benchmark_stencil(STENCIL)
-    nz = 16
-    g = orc.random_grid((nz, NY, NX), np.float32, 0)
-    cf = st["coeffs"].astype(np.float32)
+    ref, st, g, cf = _ref_block(CPU_BLOCK_NZ)
+    upd = (CPU_BLOCK_NZ - 2) * NX * NY
     for _ in range(args.warmup):
-        ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128)
+        _ref_sweep_seconds(ref, st, g, cf, 0)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        rc, _, _ = ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128)
-        assert rc == 0
+        _ref_sweep_seconds(ref, st, g, cf, 0)
     dt = time.perf_counter() - t0
-    value = g.size * args.steps / dt / 1e9
-    sample = (f"each step: 1 sweep of 3d7pt f32 on a {NX}x{NY}x{nz} block of the workload "
-              f"(seed 0), ssam::stencil3d from oracle/_ref, threads=0")
+    value = upd * args.steps / dt / 1e9
+    sample = (f"each step: 1 sweep of ssam::stencil3d<float> 3d7pt (oracle/_ref, threads=0 = "
+              f"{ref.max_threads()} threads) on global planes 0..{CPU_BLOCK_NZ - 1} of the seed-0 "
+              f"workload grid ({CPU_BLOCK_NZ - 2} planes of {NX}x{NY} updated and counted)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GCells/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -223,18 +237,56 @@ def reduce_host(x: float, op: str) -> float:
 
 
 def workload_config(world: int, args):
+    """The workload (identical for both arms); engine choices are reported
+    separately under "engine"."""
     return {"workload": f"{STENCIL} f32 {NX}x{NY}x({NZ_PER_GPU}*N) z-slab, NVLink halo exchange",
             "stencil": STENCIL, "nx": NX, "ny": NY, "nz": NZ_PER_GPU * world,
             "nz_per_gpu": NZ_PER_GPU, "iters_per_step": args.iters,
-            "temporal_block": max(1, args.tb),
-            "temporal_blocking": ("each launch fuses temporal_block sweeps (one HBM pass, "
-                                  "bit-identical to single sweeps), as ssam_b200_stencil3d_run "
-                                  "does for this stencil; --tb 1 times single sweeps"),
-            "halo": ("kernel stores into neighbours' CUDA IPC buffers (peer.py)"
-                     if args.halo == "peer" and world > 1 else
-                     "boundary planes first, NCCL send/recv overlapped with the interior"),
             "parallelism": f"z-slab x{world}", "seed": 0,
             "l2": "no flush needed: 8 GiB per buffer >> 126 MB L2"}
+
+
+def engine_config(world: int, args, tb: int):
+    return {"temporal_block": tb,
+            "temporal_blocking": ("each launch of star3d_kernel fuses temporal_block sweeps (one "
+                                  "HBM pass, bit-identical to single sweeps), as "
+                                  "ssam_b200_stencil3d_run does for this stencil; --tb 1 times "
+                                  "single sweeps"),
+            "halo": ("kernel stores into neighbours' CUDA IPC buffers (peer.py)"
+                     if args.halo == "peer" and world > 1 else
+                     "boundary planes first, NCCL send/recv overlapped with the interior")}
+
+
+def measure_traffic(tb: int, timeout: float = 240.0):
+    """dram__bytes_read.sum + dram__bytes_write.sum of one dominant-kernel
+    launch on the headline slab, from ncu run on THIS build (a subprocess:
+    the number is traffic only, never a timing)."""
+    import csv
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, "ncu not found"
+    kind = ["st3dtb", STENCIL, "f32", str(NX), str(NZ_PER_GPU + 2 * tb), str(tb)] if tb > 1 \
+        else ["st3d", STENCIL, "f32", str(NX), str(NZ_PER_GPU + 2)]
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--csv", "-k", "regex:star3d", "-s", "1", "-c", "1", sys.executable,
+           os.path.join(ROOT, "tools", "prof_one.py")] + kind
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout).stdout
+    except Exception as ex:
+        return None, f"ncu failed: {type(ex).__name__}"
+    vals = {}
+    for row in csv.reader(out.splitlines()):
+        if len(row) > 3 and row[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(row[-2], None)
+            try:
+                vals[row[-3]] = float(row[-1].replace(",", "")) * (scale or 1)
+            except ValueError:
+                pass
+    if len(vals) != 2:
+        return None, "ncu output not parsed"
+    return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]), \
+        f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum, {' '.join(kind)}"
 
 
 # ---------------------------------------------------------------------------
@@ -253,7 +305,8 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     peak, peak_kind, sm_max_nominal = load_peaks()
     st = ssam.convert_stencil(ssam.make_benchmark_stencil(STENCIL), np.float32)
     k = st.order
-    tb = max(1, args.tb)
+    # --tb 0: the depth the product's ssam_b200_stencil3d_run uses for this stencil
+    tb = args.tb if args.tb > 0 else dev.stencil3d_tb_max(st, np.float32)
     slab = decompose(NZ_PER_GPU * world, world, rank, k, ghost=k * tb)
     peer = args.halo == "peer" and world > 1
     if peer:  # the kernels store the halo into the neighbours' IPC-mapped buffers
@@ -272,32 +325,26 @@ def run_ours(args, rank: int, world: int, local_rank: int):
 
     launch_ms = []
     timing = {"on": False}
-
-    def sweep(cur, nxt, zb, ze):
-        if ze <= zb:
-            return
-        if timing["on"] and zb == slab.compute_range()[0] and world == 1:
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            dev.stencil3d_sweep(cur, nxt, st, zb, ze)
-            e.record()
-            launch_ms.append((s, e))
-        else:
-            dev.stencil3d_sweep(cur, nxt, st, zb, ze)
-
+    lo, hi = slab.compute_range()
     rlo, rhi = slab.ring_bounds()
 
-    def fused(cur, nxt, zb, ze):
-        if ze <= zb:
-            return
-        if timing["on"] and zb == slab.compute_range()[0] and world == 1:
+    def timed_launch(fn, zb):
+        if timing["on"] and zb == lo and world == 1:
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
-            dev.stencil3d_tb(cur, nxt, st, tb, zb, ze, rlo, rhi)
+            fn()
             e.record()
             launch_ms.append((s, e))
         else:
-            dev.stencil3d_tb(cur, nxt, st, tb, zb, ze, rlo, rhi)
+            fn()
+
+    def sweep(cur, nxt, zb, ze):
+        if ze > zb:
+            timed_launch(lambda: dev.stencil3d_sweep(cur, nxt, st, zb, ze), zb)
+
+    def fused(cur, nxt, zb, ze):
+        if ze > zb:
+            timed_launch(lambda: dev.stencil3d_tb(cur, nxt, st, tb, zb, ze, rlo, rhi), zb)
 
     runner = SlabRunner(slab, sweep, comm_stream=comm, fused=fused if tb > 1 else None, tb=tb)
 
@@ -342,19 +389,43 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     total_cells = NX * NY * NZ_PER_GPU * world * args.iters * args.steps
     value = total_cells / (max_ms / 1e3) / 1e9
 
-    # dominant kernel: ssam3d_kernel over the whole slab (N=1 timing by launch)
+    # dominant kernel: one launch over the whole slab (N=1 timing by launch)
     interior = (NX - 2 * k) * (NY - 2 * k)
-    lo, hi = slab.compute_range()
     cells_per_launch = interior * (hi - lo)
-    if launch_ms:
-        durs = [s.elapsed_time(e) for s, e in launch_ms]
+    fused_launches = [(s_, e_) for s_, e_ in launch_ms]
+    if fused_launches:
+        durs = [s_.elapsed_time(e_) for s_, e_ in fused_launches]
+        # a run of iters % tb trailing single sweeps is not the dominant kernel
+        if tb > 1 and args.iters % tb:
+            per_step = args.iters // tb + args.iters % tb
+            durs = [d for i, d in enumerate(durs) if i % per_step < args.iters // tb]
         mean_ms = sum(durs) / len(durs)
     else:
-        mean_ms = max_ms / (args.steps * args.iters / tb)
-    # a fused launch reads and writes every cell once for its tb updates
+        mean_ms = max_ms / (args.steps * max(1, args.iters // tb))
+    # a launch reads and writes every cell once for its tb updates
     achieved = 8.0 * cells_per_launch / (mean_ms / 1e3) / 1e9
-    traffic = load_traffic().get(f"ssam3d_{STENCIL}_f32_{NX}x{NY}x{slab.nz_local}"
-                                 + ("_tb2" if tb > 1 else ""))
+
+    # ---- per-cell parity of one step at N=1 (the product run vs the
+    # direct-gather kernels, the oracle's order and arithmetic on the GPU)
+    parity = None
+    ref_result = None
+    if world == 1 and not args.no_parity:
+        fill_slab(a, slab, NX, NY, seed=0)
+        b.copy_(a)
+        res = runner.run(a, b, args.iters)
+        g0 = torch.empty((NZ_PER_GPU, NY, NX), dtype=torch.float32, device="cuda")
+        dev.fill_random(g0, 0)
+        g1 = torch.empty_like(g0)
+        want = dev.gather_run(g0, g1, st, args.iters)
+        got = res[slab.local(0):slab.local(0) + NZ_PER_GPU]
+        rel, ab = dev.max_rel_err(got, want)
+        torch.cuda.synchronize()
+        parity = {"max_rel": rel, "max_abs": ab, "tolerance": 1e-5, "pass": rel <= 1e-5,
+                  "cells": NX * NY * NZ_PER_GPU, "iters": args.iters,
+                  "vs": "ssam_b200_gather_stencil_run (one thread per cell, the oracle's tap "
+                        "order in double, oracle.hpp:77-116) on the full grid, every cell"}
+        ref_result = got.clone()
+        del g0, g1, want, got, res
 
     # free the slab before the e2e / per-kernel phases
     del a, b
@@ -365,23 +436,29 @@ def run_ours(args, rank: int, world: int, local_rank: int):
     e2e = None
     if not args.no_e2e:
         try:
-            e2e = e2e_slab(args, slab, st, world, rank)
+            e2e = e2e_run(args, slab, st, world, rank, tb, ref_result)
         except Exception as ex:  # e.g. pinned host memory exhausted on a big box
             e2e = {"value": None, "unit": "GCells/s", "error": f"{type(ex).__name__}: {ex}"[:300]}
             torch.cuda.empty_cache()
+    del ref_result
+    ssam.lib.ssam_b200_trim_cache()
+    torch.cuda.empty_cache()
 
     kernels = None
     cpu = None
     if rank == 0 and world == 1 and not args.no_suite:
         kernels = kernel_suite(peak, sm_max_nominal)
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and not args.no_cpu:
         try:
-            v, cores, sample = reference_sample(args.cpu_seconds)
-            cpu = {"value": round(v, 6), "unit": "GCells/s", "cores": cores, "kind": "reference",
-                   "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+            cpu = reference_sample()
         except Exception as ex:  # the reference build may be absent
             cpu = {"value": None, "unit": "GCells/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
+    traffic, traffic_how = None, "skipped (--no-traffic)"
+    if rank == 0 and not args.no_traffic:
+        traffic, traffic_how = measure_traffic(tb)
+    if world > 1:
+        barrier()
 
     if rank == 0:
         line = {
@@ -391,84 +468,135 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference SplitMix64 stream, seed 0, generated on device)",
             "config": workload_config(world, args),
+            "engine": engine_config(world, args, tb),
             "hbm_gbs_algorithmic": round(value * 8.0 / tb, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic, "peak_kind": peak_kind,
-                         "kernel": (f"ssam3d_tb2_kernel {STENCIL} f32 (Tb=2: 8 B per "
-                                    f"cell per launch = 2 updates)" if tb > 1
-                                    else f"ssam3d_halo_kernel {STENCIL} f32"),
+                         "traffic": traffic, "traffic_how": traffic_how, "peak_kind": peak_kind,
+                         "kernel": (f"star3d_kernel<float, TB={tb}> {STENCIL} (8 B per interior "
+                                    f"cell per launch = {tb} updates)"),
                          "bytes_per_launch": 8 * cells_per_launch,
                          "mean_launch_ms": round(mean_ms, 4)},
+            "parity": parity,
+            "max_rel": parity["max_rel"] if parity else None,
+            "max_abs": parity["max_abs"] if parity else None,
             "e2e": e2e, "gpu_launches": int(n_launches), "clocks": clk,
             "cpu_baseline": cpu, "kernels": kernels,
         }
         print(json.dumps(line), flush=True)
 
 
-def e2e_slab(args, slab, st, world, rank):
-    """Public-API end to end: pinned host input -> GPU -> host output per step."""
+def e2e_run(args, slab, st, world, rank, tb, ref_result):
+    """Public-API end to end: pinned host input -> GPU -> host output per step.
+
+    N = 1: the C ABI on the 512-plane global grid (not the ghost-padded
+    slab).  Headline: ssam_b200_stencil_batch over `--e2e-steps` steps (each
+    step's H2D, sweeps and D2H on their own streams, so step k+1's input
+    copy and step k-1's result copy run under step k's sweeps); also the
+    one-call-per-step ssam_b200_stencil3d number.  The result is compared
+    bit for bit with the device-resident run's.
+    N > 1: the slab runner with host buffers."""
+    import ctypes
     import numpy as np
     import torch
     import paper_1907_06154_b200 as ssam
-    from paper_1907_06154_b200.slab import SlabRunner
+    from paper_1907_06154_b200.slab import SlabRunner, fill_slab
     from paper_1907_06154_b200 import device as dev
 
+    steps = max(1, args.e2e_steps)
+    if world == 1:
+        shape = (NZ_PER_GPU, NY, NX)
+        host_in = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        outs = [torch.empty(shape, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        tmp = torch.empty(shape, dtype=torch.float32, device="cuda")
+        dev.fill_random(tmp, 0)
+        host_in.copy_(tmp)
+        del tmp
+        torch.cuda.empty_cache()
+        cfg = ssam.KernelConfig(p=2, b=128)._c()
+        sa = ssam._StencilArgs(st, np.float32)
+        nbytes = host_in.numel() * 4
+
+        def single():
+            ssam._raise(ssam.lib.ssam_b200_stencil3d(
+                0, host_in.data_ptr(), NX, NY, NZ_PER_GPU, sa.ref, ctypes.byref(cfg), args.iters,
+                outs[0].data_ptr(), None))
+
+        single()  # warm-up (pool allocation, first touch of pinned pages)
+        same = None
+        if ref_result is not None:
+            chk = outs[0].to("cuda", non_blocking=False)
+            same = bool(torch.equal(chk, ref_result))
+            del chk
+            torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            single()
+        dt1 = time.perf_counter() - t0
+
+        def batch(n):
+            ssam.stencil_batch([host_in] * n, [outs[i % 2] for i in range(n)], st, args.iters,
+                               depth=2)
+
+        batch(2)  # warm-up of the batch buffers
+        t0 = time.perf_counter()
+        batch(steps)
+        dtb = time.perf_counter() - t0
+        same_b = None
+        if ref_result is not None:
+            chk = outs[(steps - 1) % 2].to("cuda", non_blocking=False)
+            same_b = bool(torch.equal(chk, ref_result))
+            del chk
+        cells = NX * NY * NZ_PER_GPU * args.iters * steps
+        return {"value": round(cells / dtb / 1e9, 3), "unit": "GCells/s",
+                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes, "steps": steps,
+                "ms_per_step": round(dtb / steps * 1e3, 3),
+                "api": ("ssam_b200_stencil_batch (C ABI, pinned host grids, copies of "
+                        "neighbouring steps overlapped with each step's sweeps)"),
+                "bit_identical_to_device_run": same_b,
+                "single_call": {"value": round(cells / dt1 / 1e9, 3), "unit": "GCells/s",
+                                "ms_per_step": round(dt1 / steps * 1e3, 3),
+                                "api": "ssam_b200_stencil3d (C ABI, one synchronous call per step)",
+                                "bit_identical_to_device_run": same}}
+
+    import torch.distributed as dist
     nzl = slab.nz_local
     host_in = torch.empty((nzl, NY, NX), dtype=torch.float32, pin_memory=True)
     host_out = torch.empty((nzl, NY, NX), dtype=torch.float32, pin_memory=True)
     tmp = torch.empty((nzl, NY, NX), dtype=torch.float32, device="cuda")
-    from paper_1907_06154_b200.slab import fill_slab
     fill_slab(tmp, slab, NX, NY, seed=0)
     host_in.copy_(tmp)
     del tmp
     torch.cuda.empty_cache()
-    steps = max(1, args.e2e_steps)
-    if world == 1:
-        import ctypes
-        cfg = ssam.KernelConfig(p=2, b=128)._c()
-        sa = ssam._StencilArgs(st, np.float32)
+    comm = torch.cuda.Stream()
+    dev_a = torch.empty((nzl, NY, NX), dtype=torch.float32, device="cuda")
+    dev_b = torch.empty_like(dev_a)
+    rlo, rhi = slab.ring_bounds()
+    runner = SlabRunner(
+        slab, lambda c, n, zb, ze: dev.stencil3d_sweep(c, n, st, zb, ze), comm_stream=comm,
+        fused=(lambda c, n, zb, ze: dev.stencil3d_tb(c, n, st, tb, zb, ze, rlo, rhi))
+        if tb > 1 else None, tb=tb)
 
-        def one():
-            ssam._raise(ssam.lib.ssam_b200_stencil3d(
-                0, host_in.data_ptr(), NX, NY, nzl, sa.ref, ctypes.byref(cfg), args.iters,
-                host_out.data_ptr(), None))
-    else:
-        import torch.distributed as dist
-        comm = torch.cuda.Stream()
-        dev_a = torch.empty((nzl, NY, NX), dtype=torch.float32, device="cuda")
-        dev_b = torch.empty_like(dev_a)
-        tb = max(1, args.tb)  # the slab carries k * tb ghost planes (run_ours)
-        rlo, rhi = slab.ring_bounds()
-        runner = SlabRunner(
-            slab, lambda c, n, zb, ze: dev.stencil3d_sweep(c, n, st, zb, ze), comm_stream=comm,
-            fused=(lambda c, n, zb, ze: dev.stencil3d_tb(c, n, st, tb, zb, ze, rlo, rhi))
-            if tb > 1 else None, tb=tb)
+    def one():
+        dev_a.copy_(host_in, non_blocking=True)
+        dev_b.copy_(dev_a)
+        res = runner.run(dev_a, dev_b, args.iters)
+        host_out.copy_(res, non_blocking=True)
+        torch.cuda.synchronize()
 
-        def one():
-            dev_a.copy_(host_in, non_blocking=True)
-            dev_b.copy_(dev_a)
-            res = runner.run(dev_a, dev_b, args.iters)
-            host_out.copy_(res, non_blocking=True)
-            torch.cuda.synchronize()
-
-    one()  # warm-up (pool allocation, first-touch of pinned pages)
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+    one()
+    dist.barrier()
     t0 = time.perf_counter()
     for _ in range(steps):
         one()
     dt = time.perf_counter() - t0
-    if world > 1:
-        dt = reduce_host(dt, "max")
+    dt = reduce_host(dt, "max")
     cells = NX * NY * NZ_PER_GPU * world * args.iters * steps
     nbytes = nzl * NY * NX * 4
     return {"value": round(cells / dt / 1e9, 3), "unit": "GCells/s",
             "h2d_bytes_per_step": nbytes * world, "d2h_bytes_per_step": nbytes * world,
             "steps": steps, "ms_per_step": round(dt / steps * 1e3, 3),
-            "api": "ssam_b200_stencil3d (C ABI, host buffers)" if world == 1 else
-                   "SlabRunner over ssam_b200_stencil3d_sweep / _tb (host buffers)"}
+            "api": "SlabRunner over ssam_b200_stencil3d_sweep / _tb (host buffers)"}
 
 
 def kernel_suite(peak, sm_mhz):
@@ -538,7 +666,7 @@ def kernel_suite(peak, sm_mhz):
                 "hbm_frac": round(gc * 2 * sz / peak, 4), "ms": round(ms, 3),
                 "tb": dev.stencil3d_tb_max(st, npdt) if name == "3d7pt" else 1}
         del a, bb
-    # the headline slab with two fused sweeps per HBM pass (engine3d_tb.cuh)
+    # the headline slab: single sweeps and the product's fused depth (engine3d_star.cuh)
     a = torch.empty((NZ_PER_GPU + 2, NY, NX), dtype=torch.float32, device="cuda")
     dev.fill_random(a, 0)
     bb = a.clone()
@@ -548,13 +676,15 @@ def kernel_suite(peak, sm_mhz):
     out[f"stencil3d_3d7pt_f32_{NX}x{NY}x{NZ_PER_GPU + 2}_tb1"] = {
         "gcells": round(gc1, 2), "hbm_gbs": round(gc1 * 8, 1),
         "hbm_frac": round(gc1 * 8 / peak, 4), "ms": round(ms1, 3), "tb": 1,
-        "note": "one sweep per launch (ssam3d_halo_kernel), 8 B/cell"}
-    ms = timed(lambda: dev.stencil3d_tb(a, bb, st, 2), 5)
-    gc = 2 * (NX - 2) * (NY - 2) * NZ_PER_GPU / ms / 1e6
-    out[f"stencil3d_3d7pt_f32_{NX}x{NY}x{NZ_PER_GPU + 2}_tb2"] = {
-        "gcells": round(gc, 2), "hbm_gbs": round(gc * 4, 1), "hbm_frac": round(gc * 4 / peak, 4),
-        "hbm_gbs_equiv": round(gc * 8, 1), "ms": round(ms, 3), "tb": 2,
-        "note": "cell-updates/s of one fused 2-sweep launch (8 B/cell per launch)"}
+        "note": "one sweep per launch (star3d_kernel TB=1), 8 B/cell"}
+    for tbk in sorted({2, dev.stencil3d_tb_max(st, np.float32)} - {1}):
+        ms = timed(lambda: dev.stencil3d_tb(a, bb, st, tbk), 5)
+        gc = tbk * (NX - 2) * (NY - 2) * NZ_PER_GPU / ms / 1e6
+        out[f"stencil3d_3d7pt_f32_{NX}x{NY}x{NZ_PER_GPU + 2}_tb{tbk}"] = {
+            "gcells": round(gc, 2), "hbm_gbs": round(gc * 8 / tbk, 1),
+            "hbm_frac": round(gc * 8 / tbk / peak, 4), "hbm_gbs_equiv": round(gc * 8, 1),
+            "ms": round(ms, 3), "tb": tbk,
+            "note": f"cell-updates/s of one fused {tbk}-sweep launch (8 B/cell per launch)"}
     del a, bb
     # 1D (kernels.hpp:390-447): conv1d 9 taps and the one-pass scan over 2^28 elements
     # (1 GiB fp32, far above L2), HBM-bound at 2 * sizeof(T) bytes per element.
@@ -585,24 +715,20 @@ def main():
     ap.add_argument("--iters", type=int, default=100, help="sweeps per step")
     ap.add_argument("--tb", type=int, default=0,
                     help="temporal block depth of the headline sweeps: 0 = what the "
-                         "product's ssam_b200_stencil3d_run uses for this stencil (2 for "
-                         "3d7pt f32: fused sweep pairs), 1 = single sweeps")
+                         "product's ssam_b200_stencil3d_run uses for this stencil, "
+                         "1 = single sweeps")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
                     help="N > 1 halo transport: NCCL send/recv, or the sweep kernel's own "
                          "stores into the neighbours' buffers (CUDA IPC / NVLink P2P)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true")
     args = ap.parse_args()
-    if args.tb <= 0:  # resolve once so both arms report the same config
-        import numpy as np
-        import paper_1907_06154_b200 as ssam
-        from paper_1907_06154_b200 import device as dev
-        st = ssam.convert_stencil(ssam.make_benchmark_stencil(STENCIL), np.float32)
-        args.tb = dev.stencil3d_tb_max(st, np.float32)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -616,6 +742,9 @@ def main():
         return
 
     if world > 1:
+        # NCCL's init log (stderr) shows the rank count and the NVLink transport
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         import torch
         import torch.distributed as dist
         dev_index = rank_device(local_rank)

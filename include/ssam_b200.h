@@ -117,6 +117,16 @@ int ssam_b200_stencil3d(int dtype, const void* in, int nx, int ny, int nz, const
                         const ssam_kernel_config* cfg, int iters, void* out,
                         ssam_op_counters* counters);
 
+/* A batch of independent grids (same shape and stencil) through the engine
+ * with the PCIe copies overlapped: grid k's host->device copy, sweeps and
+ * device->host copy run on three streams while neighbouring grids are in
+ * other stages, `depth` grids in flight (0: 2), each with two device
+ * buffers.  Results equal `count` calls of ssam_b200_stencil2d/3d (no
+ * config checks, no counters); pinned host buffers give the overlap.  2D
+ * stencils pass nz = 1.  Blocks until every result is on the host. */
+int ssam_b200_stencil_batch(int dtype, int count, const void* const* in, void* const* out, int nx,
+                            int ny, int nz, const ssam_stencil* st, int iters, int depth);
+
 /* Validation only (no device needed): the status the call above would
  * return for these arguments before touching the GPU. */
 int ssam_b200_check_conv2d(int width, int height, int m, int n, const ssam_kernel_config* cfg);
@@ -297,6 +307,16 @@ int ssam_b200_gather_conv2d(int dtype, const void* in, int width, int height, co
                             int m, int n, int boundary, void* out);
 int ssam_b200_gather_stencil(int dtype, const void* in, int nx, int ny, int nz,
                              const ssam_stencil* st, int iters, void* out);
+/* The same gather sweeps on DEVICE buffers (d_a holds the input, d_b is
+ * scratch; *d_result is whichever holds the result), stream-ordered: the
+ * per-cell check of full-size device-resident runs (bench max_rel). */
+int ssam_b200_gather_stencil_run(int dtype, void* d_a, void* d_b, int nx, int ny, int nz,
+                                 const ssam_stencil* st, int iters, void* stream,
+                                 void** d_result);
+
+/* Returns the device memory the host-grid calls keep cached in the engine's
+ * own stream-ordered pool (one per device; the default pool is untouched). */
+int ssam_b200_trim_cache(void);
 
 #ifdef __cplusplus
 }

@@ -144,6 +144,9 @@ _sig("ssam_b200_sgrd_read", [C.c_char_p, _i, _i, _p, _p, _sz, _i, _p])
 _sig("ssam_b200_sgrd_write", [C.c_char_p, _i, _i, _p, _p, _i, _p])
 _sig("ssam_b200_gather_conv2d", [_i, _p, _i, _i, _p, _i, _i, _i, _p])
 _sig("ssam_b200_gather_stencil", [_i, _p, _i, _i, _i, _PS, _i, _p])
+_sig("ssam_b200_gather_stencil_run", [_i, _p, _p, _i, _i, _i, _PS, _i, _p, C.POINTER(_p)])
+_sig("ssam_b200_trim_cache", [])
+_sig("ssam_b200_stencil_batch", [_i, _i, C.POINTER(_p), C.POINTER(_p), _i, _i, _i, _PS, _i, _i])
 
 
 class _PeerHalo(C.Structure):
@@ -179,7 +182,8 @@ EXPORTED = [
     "ssam_b200_gather_conv2d", "ssam_b200_gather_stencil", "ssam_b200_stencil3d_tb",
     "ssam_b200_stencil3d_tb_max", "ssam_b200_stencil3d_sweep_peer", "ssam_b200_stencil3d_tb_peer",
     "ssam_b200_ipc_alloc", "ssam_b200_ipc_free", "ssam_b200_ipc_open", "ssam_b200_ipc_close",
-    "ssam_b200_stencil2d_tb_range",
+    "ssam_b200_stencil2d_tb_range", "ssam_b200_gather_stencil_run", "ssam_b200_trim_cache",
+    "ssam_b200_stencil_batch",
 ]
 
 
@@ -436,6 +440,43 @@ def stencil3d(grid: np.ndarray, st: Stencil, cfg: Optional[KernelConfig] = None,
     if counters is not None:
         counters._store(cnt)
     return out
+
+
+def stencil_batch(grids, outs, st: Stencil, iters: int, depth: int = 0) -> None:
+    """ssam_b200_stencil_batch: `iters` sweeps of each grid in `grids` into the
+    matching `outs` entry, with host<->device copies overlapped across grids.
+    Grids are numpy arrays or host tensors (pinned for the overlap) of one
+    shape and dtype; 2D grids are (H, W), 3D (nz, ny, nx)."""
+    if len(grids) != len(outs):
+        raise InvalidArgument("stencil_batch: grids and outs differ in length")
+    if not grids:
+        return
+
+    def info(a):
+        if isinstance(a, np.ndarray):
+            if not a.flags.c_contiguous:
+                raise InvalidArgument("stencil_batch: grids must be C-contiguous")
+            return a.ctypes.data, a.shape, np.dtype(a.dtype)
+        return a.data_ptr(), tuple(a.shape), np.dtype(str(a.dtype).replace("torch.", ""))
+
+    ins = [info(a) for a in grids]
+    ots = [info(a) for a in outs]
+    shape, dt = ins[0][1], ins[0][2]
+    if any(i[1] != shape or i[2] != dt for i in ins + ots):
+        raise InvalidArgument("stencil_batch: every grid needs the same shape and dtype")
+    if dt not in _DT:
+        raise InvalidArgument(f"unsupported dtype {dt}")
+    if len(shape) == 2:
+        (ny, nx), nz = shape, 1
+    else:
+        nz, ny, nx = shape
+    sa = _StencilArgs(st, dt)
+    n = len(grids)
+    pin = (C.c_void_p * n)(*[i[0] for i in ins])
+    pout = (C.c_void_p * n)(*[o[0] for o in ots])
+    _raise(_lib.ssam_b200_stencil_batch(_DT[dt], n, C.cast(pin, C.POINTER(C.c_void_p)),
+                                        C.cast(pout, C.POINTER(C.c_void_p)), nx, ny, nz, sa.ref,
+                                        iters, depth))
 
 
 def _vector(a) -> np.ndarray:

@@ -312,27 +312,48 @@ int device_ready() {
     }
   });
   if (count <= 0) return fail(SSAM_ERR_NO_DEVICE, "no CUDA device available");
-  // Keep freed stream-ordered allocations cached in the pool: repeated host
-  // calls then reuse device buffers instead of re-mapping memory.
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return cuda_fail(cudaGetLastError(), "cudaGetDevice");
-  static std::once_flag pool_once[64];
-  if (dev >= 0 && dev < 64)
-    std::call_once(pool_once[dev], [dev] {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        std::uint64_t thr = std::numeric_limits<std::uint64_t>::max();
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-    });
   return SSAM_OK;
+}
+
+// The engine's own stream-ordered pool per device: freed staging buffers of
+// the host-grid calls stay cached (repeated calls reuse them instead of
+// re-mapping memory) without touching the device's default pool, which torch
+// and other cudaMallocAsync users share.  ssam_b200_trim_cache() returns the
+// cached memory.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+cudaMemPool_t engine_pool() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    std::uint64_t thr = std::numeric_limits<std::uint64_t>::max();
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    g_pools[dev] = pool;
+  }
+  return g_pools[dev];
 }
 
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t s;
   explicit DevBuf(cudaStream_t st) : s(st) {}
-  cudaError_t alloc(size_t bytes) { return cudaMallocAsync(&p, bytes, s); }
+  cudaError_t alloc(size_t bytes) {
+    cudaMemPool_t pool = engine_pool();
+    return pool ? cudaMallocFromPoolAsync(&p, bytes, pool, s) : cudaMallocAsync(&p, bytes, s);
+  }
   ~DevBuf() {
     if (p) cudaFreeAsync(p, s);
   }
@@ -673,6 +694,97 @@ int push_planes(int dtype, void* d_out, int nx, int ny, int z0, int z1, const Pe
 }  // namespace
 
 // ===========================================================================
+namespace {
+// Device-resident direct-gather sweeps (the oracle's order and arithmetic):
+// the per-cell verifier of full-size device runs (bench max_rel, GPU tests).
+template <class T>
+cudaError_t gather_run(T* a, T* b, int nx, int ny, int nz, const StencilDesc<T>& d, int iters,
+                       cudaStream_t s, T** result) {
+  const size_t bytes = static_cast<size_t>(nx) * ny * nz * sizeof(T);
+  cudaError_t e = cudaMemcpyAsync(b, a, bytes, cudaMemcpyDeviceToDevice, s);  // the ring
+  T* cur = a;
+  T* nxt = b;
+  for (int it = 0; e == cudaSuccess && it < iters; ++it) {
+    e = d.dims == 2 ? stencil2d_direct<T>(cur, nxt, nx, ny, 0, ny, d, s)
+                    : stencil3d_direct<T>(cur, nxt, nx, ny, nz, 0, nz, d, s);
+    std::swap(cur, nxt);
+  }
+  *result = cur;
+  return e;
+}
+
+}  // namespace
+
+namespace {
+// Many independent grids through the engine with the copies overlapped:
+// grid k's H2D (copy stream), sweeps (compute stream) and D2H (copy-back
+// stream) run while grid k-1 is being computed / copied back, `depth` grids
+// in flight, each with its own pair of device buffers.
+template <class T>
+int host_stencil_batch(int count, const void* const* in, void* const* out, int nx, int ny, int nz,
+                       const ssam_stencil* st, int iters, int depth) {
+  const size_t bytes = static_cast<size_t>(nx) * ny * nz * sizeof(T);
+  const StencilDesc<T> d = make_desc<T>(st);
+  const int dtype = sizeof(T) == 4 ? SSAM_DTYPE_F32 : (std::is_same<T, double>::value ? 1 : 2);
+  depth = std::max(1, std::min(depth, count));
+  struct Res {
+    cudaStream_t s[3] = {};
+    std::vector<cudaEvent_t> ev;
+    std::vector<void*> buf;
+    ~Res() {
+      for (cudaStream_t x : s)
+        if (x) cudaStreamSynchronize(x);
+      for (void* p : buf)
+        if (p) cudaFreeAsync(p, s[1]);
+      if (s[1]) cudaStreamSynchronize(s[1]);
+      for (cudaEvent_t e : ev)
+        if (e) cudaEventDestroy(e);
+      for (cudaStream_t x : s)
+        if (x) cudaStreamDestroy(x);
+    }
+  } r;
+  cudaError_t e = cudaSuccess;
+  for (cudaStream_t& x : r.s)
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking);
+  r.ev.assign(3 * depth, nullptr);
+  for (cudaEvent_t& x : r.ev)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  r.buf.assign(2 * depth, nullptr);
+  cudaMemPool_t pool = engine_pool();
+  for (void*& p : r.buf)
+    if (e == cudaSuccess)
+      e = pool ? cudaMallocFromPoolAsync(&p, bytes, pool, r.s[1]) : cudaMallocAsync(&p, bytes, r.s[1]);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(r.s[1]);
+  if (e != cudaSuccess) return cuda_fail(e, "stencil batch setup");
+  cudaEvent_t* ev_in = r.ev.data();            // input landed
+  cudaEvent_t* ev_done = r.ev.data() + depth;  // result computed
+  cudaEvent_t* ev_out = r.ev.data() + 2 * depth;  // result copied back (slot free)
+  for (int k = 0; k < count && e == cudaSuccess; ++k) {
+    const int sl = k % depth;
+    T* a = static_cast<T*>(r.buf[2 * sl]);
+    T* b = static_cast<T*>(r.buf[2 * sl + 1]);
+    if (k >= depth) e = cudaStreamWaitEvent(r.s[0], ev_out[sl], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(a, in[k], bytes, cudaMemcpyHostToDevice, r.s[0]);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_in[sl], r.s[0]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(r.s[1], ev_in[sl], 0);
+    T* res = nullptr;
+    if (e == cudaSuccess)
+      e = st->dims == 2 ? run2d<T>(a, b, nx, ny, d, iters, default_tb(dtype, st), r.s[1], &res)
+                        : run3d<T>(a, b, nx, ny, nz, d, iters, r.s[1], &res);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_done[sl], r.s[1]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(r.s[2], ev_done[sl], 0);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out[k], res, bytes, cudaMemcpyDeviceToHost, r.s[2]);
+    if (e == cudaSuccess) e = cudaEventRecord(ev_out[sl], r.s[2]);
+  }
+  for (cudaStream_t x : r.s)
+    if (e == cudaSuccess) e = cudaStreamSynchronize(x);
+  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "stencil batch");
+}
+template <class T> struct HostBatch {
+  template <class... A> static int run(A... a) { return host_stencil_batch<T>(a...); }
+};
+}  // namespace
+
 extern "C" {
 
 int ssam_b200_abi_version(void) { return SSAM_B200_ABI_VERSION; }
@@ -776,6 +888,22 @@ int ssam_b200_stencil3d(int dtype, const void* in, int nx, int ny, int nz, const
   if (int s = by_dtype<HostStencil>(dtype, in, nx, ny, nz, st, iters, out)) return s;
   if (counters) counters_stencil3d(nx, ny, nz, st, c, iters, counters);
   return SSAM_OK;
+}
+
+int ssam_b200_stencil_batch(int dtype, int count, const void* const* in, void* const* out, int nx,
+                            int ny, int nz, const ssam_stencil* st, int iters, int depth) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = validate_stencil(st)) return s;
+  if (st->dims == 2) nz = 1;
+  const int m = 2 * st->order + 1;
+  if (count < 0 || !in || !out || iters < 0 || nx < m || ny < m || (st->dims == 3 && nz < m))
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil_batch: bad arguments");
+  for (int k = 0; k < count; ++k)
+    if (!in[k] || !out[k]) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil_batch: null grid");
+  if (count == 0) return SSAM_OK;
+  if (int s = device_ready()) return s;
+  return by_dtype<HostBatch>(dtype, count, in, out, nx, ny, nz, st, iters, depth <= 0 ? 2 : depth);
 }
 
 int ssam_b200_benchmark_count(void) { return kNumBench; }
@@ -936,16 +1064,23 @@ int ssam_b200_stencil2d_run(int dtype, void* d_a, void* d_b, int w, int h, const
   if (int s = validate_stencil(st)) return s;
   if (st->dims != 2) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil2d: needs a 2D stencil");
   if (iters < 0) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil2d: iters must be >= 0");
+  if (!d_a || !d_b || !d_result || d_a == d_b)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil2d_run: null or aliased buffer");
+  if (w < 2 * st->order + 1 || h < 2 * st->order + 1)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil2d_run: domain smaller than 2k+1");
   if (int s = device_ready()) return s;
   if (tb <= 0) tb = default_tb(dtype, st);
   cudaError_t e = cudaErrorInvalidValue;
   const cudaStream_t s = as_stream(stream);
+  void* r = nullptr;
   switch (dtype) {
-    case 0: { float* r; e = run2d<float>(static_cast<float*>(d_a), static_cast<float*>(d_b), w, h, make_desc<float>(st), iters, tb, s, &r); *d_result = r; break; }
-    case 1: { double* r; e = run2d<double>(static_cast<double*>(d_a), static_cast<double*>(d_b), w, h, make_desc<double>(st), iters, tb, s, &r); *d_result = r; break; }
-    case 2: { long long* r; e = run2d<long long>(static_cast<long long*>(d_a), static_cast<long long*>(d_b), w, h, make_desc<long long>(st), iters, tb, s, &r); *d_result = r; break; }
+    case 0: { float* q = nullptr; e = run2d<float>(static_cast<float*>(d_a), static_cast<float*>(d_b), w, h, make_desc<float>(st), iters, tb, s, &q); r = q; break; }
+    case 1: { double* q = nullptr; e = run2d<double>(static_cast<double*>(d_a), static_cast<double*>(d_b), w, h, make_desc<double>(st), iters, tb, s, &q); r = q; break; }
+    case 2: { long long* q = nullptr; e = run2d<long long>(static_cast<long long*>(d_a), static_cast<long long*>(d_b), w, h, make_desc<long long>(st), iters, tb, s, &q); r = q; break; }
   }
-  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "stencil2d_run");
+  if (e != cudaSuccess) return cuda_fail(e, "stencil2d_run");
+  *d_result = r;
+  return SSAM_OK;
 }
 
 int ssam_b200_stencil3d_run(int dtype, void* d_a, void* d_b, int nx, int ny, int nz,
@@ -955,15 +1090,54 @@ int ssam_b200_stencil3d_run(int dtype, void* d_a, void* d_b, int nx, int ny, int
   if (int s = validate_stencil(st)) return s;
   if (st->dims != 3) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d: needs a 3D stencil");
   if (iters < 0) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d: iters must be >= 0");
+  if (!d_a || !d_b || !d_result || d_a == d_b)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d_run: null or aliased buffer");
+  const int m = 2 * st->order + 1;
+  if (nx < m || ny < m || nz < m)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d_run: domain smaller than 2k+1");
   if (int s = device_ready()) return s;
   cudaError_t e = cudaErrorInvalidValue;
   const cudaStream_t s = as_stream(stream);
+  void* r = nullptr;
   switch (dtype) {
-    case 0: { float* r; e = run3d<float>(static_cast<float*>(d_a), static_cast<float*>(d_b), nx, ny, nz, make_desc<float>(st), iters, s, &r); *d_result = r; break; }
-    case 1: { double* r; e = run3d<double>(static_cast<double*>(d_a), static_cast<double*>(d_b), nx, ny, nz, make_desc<double>(st), iters, s, &r); *d_result = r; break; }
-    case 2: { long long* r; e = run3d<long long>(static_cast<long long*>(d_a), static_cast<long long*>(d_b), nx, ny, nz, make_desc<long long>(st), iters, s, &r); *d_result = r; break; }
+    case 0: { float* q = nullptr; e = run3d<float>(static_cast<float*>(d_a), static_cast<float*>(d_b), nx, ny, nz, make_desc<float>(st), iters, s, &q); r = q; break; }
+    case 1: { double* q = nullptr; e = run3d<double>(static_cast<double*>(d_a), static_cast<double*>(d_b), nx, ny, nz, make_desc<double>(st), iters, s, &q); r = q; break; }
+    case 2: { long long* q = nullptr; e = run3d<long long>(static_cast<long long*>(d_a), static_cast<long long*>(d_b), nx, ny, nz, make_desc<long long>(st), iters, s, &q); r = q; break; }
   }
-  return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "stencil3d_run");
+  if (e != cudaSuccess) return cuda_fail(e, "stencil3d_run");
+  *d_result = r;
+  return SSAM_OK;
+}
+
+int ssam_b200_gather_stencil_run(int dtype, void* d_a, void* d_b, int nx, int ny, int nz,
+                                 const ssam_stencil* st, int iters, void* stream,
+                                 void** d_result) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  if (int s = validate_stencil(st)) return s;
+  if (st->dims == 2) nz = 1;
+  if (nx < 1 || ny < 1 || nz < 1 || iters < 0 || !d_a || !d_b || !d_result || d_a == d_b)
+    return fail(SSAM_ERR_INVALID_ARGUMENT, "gather_stencil_run: bad arguments");
+  if (int s = device_ready()) return s;
+  cudaError_t e = cudaErrorInvalidValue;
+  const cudaStream_t s = as_stream(stream);
+  void* r = nullptr;
+  switch (dtype) {
+    case 0: { float* q = nullptr; e = gather_run<float>(static_cast<float*>(d_a), static_cast<float*>(d_b), nx, ny, nz, make_desc<float>(st), iters, s, &q); r = q; break; }
+    case 1: { double* q = nullptr; e = gather_run<double>(static_cast<double*>(d_a), static_cast<double*>(d_b), nx, ny, nz, make_desc<double>(st), iters, s, &q); r = q; break; }
+    case 2: { long long* q = nullptr; e = gather_run<long long>(static_cast<long long*>(d_a), static_cast<long long*>(d_b), nx, ny, nz, make_desc<long long>(st), iters, s, &q); r = q; break; }
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "gather_stencil_run");
+  *d_result = r;
+  return SSAM_OK;
+}
+
+int ssam_b200_trim_cache(void) {
+  g_err.clear();
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (cudaMemPool_t p : g_pools)
+    if (p && cudaMemPoolTrimTo(p, 0) != cudaSuccess) return cuda_fail(cudaGetLastError(), "trim_cache");
+  return SSAM_OK;
 }
 
 int ssam_b200_fill_random(int dtype, void* d_out, size_t count, uint64_t seed, uint64_t first,

@@ -82,7 +82,13 @@ struct StarGeom {
   }
   static constexpr int CWARPS = first_warp(TB + 1);
   static constexpr int THREADS = 32 * (CWARPS + 1);  // + the TMA producer warp
-  static constexpr int DZ = 4, DI = 4;                // input / intermediate ring depth
+#ifndef SSAM_STAR_DZ
+#define SSAM_STAR_DZ 6
+#endif
+#ifndef SSAM_STAR_DI
+#define SSAM_STAR_DI 3
+#endif
+  static constexpr int DZ = SSAM_STAR_DZ, DI = SSAM_STAR_DI;  // input / intermediate ring depth
   static constexpr int cmax(int a, int b) { return a > b ? a : b; }
   static constexpr int IN_ROWS = cmax(sy(1) * ry(1) + 2, nr(1) + 2);
   // slot rows of the ring between stage s and s+1: written by s, read by s+1
@@ -97,7 +103,10 @@ struct StarGeom {
   }
   static constexpr size_t BAR_OFF = mid_off(TB);
   static constexpr size_t SMEM = BAR_OFF + (2 * DZ + 2 * DI * (TB - 1)) * 8;
-  static constexpr int MINB = TB == 1 ? 3 : (TB == 2 ? 2 : 1);
+#ifndef SSAM_STAR_MINB2
+#define SSAM_STAR_MINB2 2
+#endif
+  static constexpr int MINB = TB == 1 ? 3 : (TB == 2 ? SSAM_STAR_MINB2 : 1);
   static_assert(IN_ROWS <= 256, "TMA box rows");
 };
 
@@ -146,16 +155,24 @@ __device__ __forceinline__ void star_stage(const Par& p, const StarCtx<T, TB>& c
     return reinterpret_cast<const T*>(src + static_cast<size_t>(j % D) * SLOT) + row0 * BW + Q * lane;
   };
   // plane j arrives: wait for it, read its RY centre rows (rows 1..RY)
+#ifndef SSAM_STAR_EAGER
+#define SSAM_STAR_EAGER 0
+#endif
+  // EAGER: all RY + 2 rows at arrival (slot released one step earlier, two
+  // more rows of registers per plane); lazy: halo rows when centre.
+  constexpr bool EAGER = SSAM_STAR_EAGER != 0;
   auto take = [&](int j, T (&dst)[NROW][Q]) {
     mbar_wait(smem_u32(&sfull[j % D]), (j / D) & 1);
     const T* sp = slot_ptr(j);
 #pragma unroll
-    for (int r = 1; r <= RY; ++r) lds_q<T, Q>(sp + r * BW, dst[r]);
+    for (int r = EAGER ? 0 : 1; r <= (EAGER ? RY + 1 : RY); ++r) lds_q<T, Q>(sp + r * BW, dst[r]);
   };
   auto halo = [&](int j, T (&dst)[NROW][Q]) {
-    const T* sp = slot_ptr(j);
-    lds_q<T, Q>(sp, dst[0]);
-    lds_q<T, Q>(sp + (RY + 1) * BW, dst[RY + 1]);
+    if constexpr (!EAGER) {
+      const T* sp = slot_ptr(j);
+      lds_q<T, Q>(sp, dst[0]);
+      lds_q<T, Q>(sp + (RY + 1) * BW, dst[RY + 1]);
+    }
   };
   auto release = [&](int j) { mbar_arrive(smem_u32(&sempty[j % D])); };
 
@@ -217,8 +234,16 @@ __device__ __forceinline__ void star_stage(const Par& p, const StarCtx<T, TB>& c
       }
     }
     if constexpr (S < TB) mbar_arrive(smem_u32(&dfull[m % G::DI]));
-    release(m + 1);  // its halo rows fed this step's FMAs; the slot may refill
-    if (m == 0) release(0);
+    if constexpr (EAGER) {
+      release(m + 2);  // every row of the new plane fed this step's FMAs
+      if (m == 0) {
+        release(0);
+        release(1);
+      }
+    } else {
+      release(m + 1);  // its halo rows fed this step's FMAs; the slot may refill
+      if (m == 0) release(0);
+    }
   };
 
   for (int mb = 0; mb < n_out; mb += 3) {
@@ -231,7 +256,7 @@ __device__ __forceinline__ void star_stage(const Par& p, const StarCtx<T, TB>& c
     take(mb + 4, pl[1]);
     step(mb + 2, pl[2], pl[0], pl[1]);
   }
-  release(n_out + 1);  // the last plane was only ever a z+1 plane
+  if constexpr (!EAGER) release(n_out + 1);  // the last plane was only ever a z+1 plane
 }
 
 template <class T, int TB, int S, bool PEER, class Par>

@@ -148,6 +148,21 @@ def stencil3d_run(d_a, d_b, st: Stencil, iters: int, stream=None):
     return d_a if res.value == d_a.data_ptr() else d_b
 
 
+def gather_run(d_a, d_b, st: Stencil, iters: int, stream=None):
+    """`iters` direct-gather sweeps (the oracle's summation order and arithmetic)
+    on device buffers; returns whichever of d_a / d_b holds the result."""
+    code = _code(d_a)
+    if d_a.dim() == 2:
+        (ny, nx), nz = d_a.shape, 1
+    else:
+        nz, ny, nx = d_a.shape
+    sa = _StencilArgs(st, _np_dtype(code))
+    res = C.c_void_p()
+    _raise(_lib.ssam_b200_gather_stencil_run(code, d_a.data_ptr(), d_b.data_ptr(), nx, ny, nz,
+                                             sa.ref, iters, _s(stream), C.byref(res)))
+    return d_a if res.value == d_a.data_ptr() else d_b
+
+
 def fill_random(t, seed: int, first: int = 0, stream=None) -> None:
     """SplitMix64 fill bit-identical to random_grid2d/3d (element i = draw first+i)."""
     _raise(_lib.ssam_b200_fill_random(_code(t), t.data_ptr(), t.numel(), seed, first,

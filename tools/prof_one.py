@@ -1,5 +1,5 @@
 """Launch one kernel config a few times (for ncu captures): prof_one.py KIND [args]
-   conv K | st2d NAME DT | st3d NAME DT N [NZ] | st3dtb NAME DT N [NZ] | conv1d M DT | scan DT"""
+   conv K | st2d NAME DT | st3d NAME DT N [NZ] | st3dtb NAME DT N [NZ [TB]] | conv1d M DT | scan DT"""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -37,10 +37,11 @@ elif kind == "st2d":
 elif kind == "st3dtb":
     name, dt, n = sys.argv[2], sys.argv[3], int(sys.argv[4])
     nz = int(sys.argv[5]) if len(sys.argv) > 5 else n
+    tb = int(sys.argv[6]) if len(sys.argv) > 6 else 2
     tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)
     a = torch.empty((nz, n, n), dtype=tdt, device="cuda"); dev.fill_random(a, 0); b = a.clone()
     st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt)
-    for _ in range(reps): dev.stencil3d_tb(a, b, st, 2)
+    for _ in range(reps): dev.stencil3d_tb(a, b, st, tb)
 else:
     name, dt, n = sys.argv[2], sys.argv[3], int(sys.argv[4])
     tdt, npdt = (torch.float32, np.float32) if dt == "f32" else (torch.float64, np.float64)

@@ -117,9 +117,31 @@ def time_all():
         print(f"2048^2x258 f64 tb={tb}: {ms:.3f} ms {tb * cells / ms / 1e6:.1f} GCells/s", flush=True)
 
 
+def quick():
+    """TB=2 timings only (A/B of build variants): 2048^2x514 f32, 512^3 f32/f64, 2048^2x258 f64."""
+    out = []
+    for npdt, tdt, shape in ((np.float32, torch.float32, (514, 2048, 2048)),
+                             (np.float32, torch.float32, (512, 512, 512)),
+                             (np.float64, torch.float64, (512, 512, 512)),
+                             (np.float64, torch.float64, (258, 2048, 2048))):
+        st = ssam.convert_stencil(ssam.make_benchmark_stencil("3d7pt"), npdt)
+        a = torch.empty(shape, dtype=tdt, device="cuda")
+        dev.fill_random(a, 0)
+        b = a.clone()
+        nz, ny, nx = shape
+        cells = (nx - 2) * (ny - 2) * (nz - 2)
+        ms = timed(lambda: dev.stencil3d_tb(a, b, st, 2), 10)
+        out.append(f"{np.dtype(npdt).name[0]}{np.dtype(npdt).itemsize * 8}:{nx}x{nz}={2 * cells / ms / 1e6:.0f}")
+        del a, b
+        torch.cuda.empty_cache()
+    print(os.environ.get("SSAM_B200_LIB", "main"), " ".join(out), flush=True)
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["check", "time"]
     if "check" in what:
         check()
     if "time" in what:
         time_all()
+    if "quick" in what:
+        quick()
