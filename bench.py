@@ -15,7 +15,7 @@ each GPU always owns 2048 x 2048 x 512 cells.
           with the device-resident result; the slab runner at N>1): pinned
           host->device copy of each step's input, the sweeps, and the
           device->host copy of its result inside the timed region.
-  roofline  the dominant kernel (star3d_kernel, TB fused sweeps per launch):
+  roofline  the dominant kernel (pipe3d_kernel, TB fused sweeps per launch):
           algorithmic bytes (4 B read + 4 B write per interior cell per
           launch) / mean launch time; traffic from ncu on this build.
   parity  every cell of one step (100 sweeps) at N=1 against the
@@ -248,7 +248,7 @@ def workload_config(world: int, args):
 
 def engine_config(world: int, args, tb: int):
     return {"temporal_block": tb,
-            "temporal_blocking": ("each launch of star3d_kernel fuses temporal_block sweeps (one "
+            "temporal_blocking": ("each launch of pipe3d_kernel fuses temporal_block sweeps (one "
                                   "HBM pass, bit-identical to single sweeps), as "
                                   "ssam_b200_stencil3d_run does for this stencil; --tb 1 times "
                                   "single sweeps"),
@@ -269,7 +269,7 @@ def measure_traffic(tb: int, timeout: float = 240.0):
     kind = ["st3dtb", STENCIL, "f32", str(NX), str(NZ_PER_GPU + 2 * tb), str(tb)] if tb > 1 \
         else ["st3d", STENCIL, "f32", str(NX), str(NZ_PER_GPU + 2)]
     cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--csv", "-k", "regex:star3d", "-s", "1", "-c", "1", sys.executable,
+           "--csv", "-k", "regex:pipe3d", "-s", "1", "-c", "1", sys.executable,
            os.path.join(ROOT, "tools", "prof_one.py")] + kind
     try:
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout).stdout
@@ -473,7 +473,7 @@ def run_ours(args, rank: int, world: int, local_rank: int):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
                          "traffic": traffic, "traffic_how": traffic_how, "peak_kind": peak_kind,
-                         "kernel": (f"star3d_kernel<float, TB={tb}> {STENCIL} (8 B per interior "
+                         "kernel": (f"pipe3d_kernel<float, PipeStar<1>, TB={tb}> {STENCIL} (8 B per interior "
                                     f"cell per launch = {tb} updates)"),
                          "bytes_per_launch": 8 * cells_per_launch,
                          "mean_launch_ms": round(mean_ms, 4)},
@@ -666,7 +666,7 @@ def kernel_suite(peak, sm_mhz):
                 "hbm_frac": round(gc * 2 * sz / peak, 4), "ms": round(ms, 3),
                 "tb": dev.stencil3d_tb_max(st, npdt) if name == "3d7pt" else 1}
         del a, bb
-    # the headline slab: single sweeps and the product's fused depth (engine3d_star.cuh)
+    # the headline slab: single sweeps and the product's fused depth (engine3d_pipe.cuh)
     a = torch.empty((NZ_PER_GPU + 2, NY, NX), dtype=torch.float32, device="cuda")
     dev.fill_random(a, 0)
     bb = a.clone()
@@ -676,7 +676,7 @@ def kernel_suite(peak, sm_mhz):
     out[f"stencil3d_3d7pt_f32_{NX}x{NY}x{NZ_PER_GPU + 2}_tb1"] = {
         "gcells": round(gc1, 2), "hbm_gbs": round(gc1 * 8, 1),
         "hbm_frac": round(gc1 * 8 / peak, 4), "ms": round(ms1, 3), "tb": 1,
-        "note": "one sweep per launch (star3d_kernel TB=1), 8 B/cell"}
+        "note": "one sweep per launch (pipe3d_kernel TB=1), 8 B/cell"}
     for tbk in sorted({2, dev.stencil3d_tb_max(st, np.float32)} - {1}):
         ms = timed(lambda: dev.stencil3d_tb(a, bb, st, tbk), 5)
         gc = tbk * (NX - 2) * (NY - 2) * NZ_PER_GPU / ms / 1e6

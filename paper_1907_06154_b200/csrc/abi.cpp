@@ -415,15 +415,14 @@ cudaError_t run3d(T* a, T* b, int nx, int ny, int nz, const StencilDesc<T>& d, i
   T* cur = a;
   T* nxt = b;
   const int dtype = sizeof(T) == 4 ? 0 : (std::is_same<T, double>::value ? 1 : 2);
-  const int tb = (d.order == 1 && classify3d(d.taps, 1) == Shape3D::star)
-                     ? stencil3d_tb_max(dtype, d.order)
-                     : 1;
+  const int tb = stencil3d_tb_max(dtype, d.order, classify3d(d.taps, d.order));
   int done = 0;
   while (done < iters) {
-    int depth = 1;
-    if (tb > 1 && iters - done >= tb) {
-      depth = tb;
-      e = stencil3d_tb<T>(cur, nxt, nx, ny, nz, 0, nz, d.order, nz - d.order, d, tb, s);
+    // full-depth fused launches, then the remainder as one shorter fused
+    // launch where a kernel exists, else single sweeps
+    int depth = std::min(tb, iters - done);
+    if (depth > 1) {
+      e = stencil3d_tb<T>(cur, nxt, nx, ny, nz, 0, nz, d.order, nz - d.order, d, depth, s);
       if (e == cudaErrorNotSupported) {
         cudaGetLastError();
         depth = 1;
@@ -1290,7 +1289,10 @@ int ssam_b200_stencil3d_tb(int dtype, const void* d_in, void* d_out, int nx, int
 
 int ssam_b200_stencil3d_tb_max(int dtype, const ssam_stencil* st) {
   if (!st || st->dims != 3 || !dtype_ok(dtype)) return 1;
-  return stencil3d_tb_max(dtype, st->order);
+  std::vector<Tap> taps;
+  for (int i = 0; i < st->ntaps; ++i)
+    taps.push_back({st->offsets[3 * i], st->offsets[3 * i + 1], st->offsets[3 * i + 2]});
+  return stencil3d_tb_max(dtype, st->order, classify3d(taps, st->order));
 }
 
 int ssam_b200_stencil3d_sweep_peer(int dtype, const void* d_in, void* d_out, int nx, int ny,

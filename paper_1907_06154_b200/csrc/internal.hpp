@@ -72,19 +72,27 @@ cudaError_t stencil3d_sweep(const T* d_in, T* d_out, int nx, int ny, int nz, int
 template <class T>
 cudaError_t stencil3d_tb(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
                          int zr_lo, int zr_hi, const StencilDesc<T>& st, int tb, cudaStream_t s);
-int stencil3d_tb_max(int dtype, int order);
 
-// ---- the order-1 3D star pipeline (star3d.cu, engine3d_star.cuh) ------------
-// coef27: host, the dense 3x3x3 layout coef[(l*3 + j)*3 + t] (l = dz+1,
-// j = dx+1, t = dy+1) with only the 7 star cells used.  star3d_tb fuses tb in
-// {2, 3, 4} sweeps; cudaErrorNotSupported for unaligned grids.
-bool star3d_enabled();
+// ---- the 3D pipeline engine (engine3d_pipe.cuh, pipe3d_*.cu) -------------
+// coef: host, the dense (2K+1)^3 layout coef[(l*M + j)*M + t] (l = dz+K,
+// j = dx+K, t = dy+K).  tb = 1 is one sweep over output planes [z_begin,
+// z_end) (aligned: the pipeline; otherwise the direct-load kernel); tb >= 2
+// fuses tb sweeps (order-1 star: 2..4; order-2 star and the box family: 2)
+// with the global ring outside planes [zr_lo, zr_hi); cudaErrorNotSupported
+// for unaligned grids or depths without a kernel.
+bool pipe3d_enabled();
 template <class T>
-cudaError_t star3d_sweep(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
-                         const T* coef27, cudaStream_t s);
+cudaError_t pipe3d_star1(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
+                         int zr_lo, int zr_hi, const T* coef, int tb, cudaStream_t s);
 template <class T>
-cudaError_t star3d_tb(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
-                      int zr_lo, int zr_hi, const T* coef27, int tb, cudaStream_t s);
+cudaError_t pipe3d_star2(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
+                         int zr_lo, int zr_hi, const T* coef, int tb, cudaStream_t s);
+template <class T>
+cudaError_t pipe3d_box(bool poisson, const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin,
+                       int z_end, int zr_lo, int zr_hi, const T* coef, int tb, cudaStream_t s);
+// The fused depth stencil3d_run uses for a (dtype, order, shape): measured
+// per shape; SSAM_B200_3D_TB caps it (1 = single sweeps).
+int stencil3d_tb_max(int dtype, int order, Shape3D shape);
 
 // ---- direct-gather kernels (generic path: any order / tap set) -------------
 // Bit-faithful to the oracle's summation order (double accumulation for FP,

@@ -54,8 +54,15 @@ cudaError_t stencil3d_dispatch(const T* d_in, T* d_out, int nx, int ny, int nz, 
   Engine3DArgs<T> a{d_in, d_out, nx, ny, nz, k, coef.data(), z_begin, z_end};
   if constexpr (SHAPES) {
     const Shape3D sh = classify3d(st.taps, k);
-    if (k == 1 && sh == Shape3D::star && star3d_enabled())
-      return star3d_sweep<T>(d_in, d_out, nx, ny, nz, z_begin, z_end, coef.data(), s);
+    if (pipe3d_enabled()) {  // the pipeline engine (engine3d_pipe.cuh)
+      if (k == 1 && sh == Shape3D::star)
+        return pipe3d_star1<T>(d_in, d_out, nx, ny, nz, z_begin, z_end, 1, nz - 1, coef.data(), 1, s);
+      if (k == 2 && sh == Shape3D::star)
+        return pipe3d_star2<T>(d_in, d_out, nx, ny, nz, z_begin, z_end, 2, nz - 2, coef.data(), 1, s);
+      if (k == 1)  // poisson, the 27-point box and any other order-1 tap set (dense)
+        return pipe3d_box<T>(sh == Shape3D::poisson, d_in, d_out, nx, ny, nz, z_begin, z_end, 1,
+                             nz - 1, coef.data(), 1, s);
+    }
     if (k == 1 && sh == Shape3D::star) return st3d<T, 1, StarMask3<1>>(a, s);
     if (k == 2 && sh == Shape3D::star) return st3d<T, 2, StarMask3<2>>(a, s);
     if (k == 1 && sh == Shape3D::poisson) return st3d<T, 1, PoissonMask3>(a, s);
@@ -92,23 +99,32 @@ bool stencil3d_peer_fused(int dtype, int order) { return order <= (dtype == 2 ? 
 
 // ---- temporal blocking (Tb = 2), engine3d_tb.cuh --------------------------------
 // SSAM_B200_3D_TB=1 disables the fused path (plain sweeps).
-inline int tb3d_max_env() {
-  static const int v = [] {
-    const char* e = std::getenv("SSAM_B200_3D_TB");
-    return e ? std::atoi(e) : 2;
+
+
+// SSAM_B200_PIPE=0 routes every 3D shape back to the generic engines below
+// (engine3d.cuh / engine3d_tb.cuh) for A/B runs.
+bool pipe3d_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SSAM_B200_PIPE");
+    return !e || std::atoi(e) != 0;
   }();
   return v;
 }
 
-// Measured (B200, bit-identical to two sweeps): 3d7pt fp32 +23% at 512^3,
-// +27..35% at 2048^2; fp64 (4-warp CTAs) +12% at 512^3, +21% at 2048^2 x 130.
-// The heavier footprints are compute-bound already and lose (poisson /
-// 3d27pt -20..30%), so only the 7-point star fuses (run3d checks the shape).
-int stencil3d_tb_max(int dtype, int order) {
-  if (dtype == 2 || order != 1) return 1;
-  const int t = tb3d_max_env();
-  if (!star3d_enabled()) return t >= 2 ? 2 : 1;
-  return std::max(1, std::min(t, 4));
+// Fused depth per shape (B200, pipeline engine, GCells/s at 512^3, single
+// sweep / Tb = 2; profiles/r02/pipe_shapes.txt): 3d7pt f32 660 / 996, f64
+// 341 / 610; 3d13pt f32 614 / 643, f64 355 / 334; 3d27pt and poisson lose
+// 30-50% fused (compute-bound, one CTA per SM).  SSAM_B200_3D_TB asks for a
+// depth (clamped to the compiled ones).
+int stencil3d_tb_max(int dtype, int order, Shape3D shape) {
+  if (dtype == 2) return 1;
+  const bool star1 = order == 1 && shape == Shape3D::star;
+  const char* e = std::getenv("SSAM_B200_3D_TB");
+  if (!pipe3d_enabled()) return (star1 && (!e || std::atoi(e) >= 2)) ? 2 : 1;
+  const int most = star1 ? 4 : (order == 1 || (order == 2 && shape == Shape3D::star)) ? 2 : 1;
+  const bool star2 = order == 2 && shape == Shape3D::star;
+  const int want = e ? std::atoi(e) : (star1 || (star2 && dtype == 0) ? 2 : 1);
+  return std::max(1, std::min(want, most));
 }
 
 template <class T, class Mask>
@@ -180,11 +196,21 @@ cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_b
 template <class T>
 cudaError_t stencil3d_tb_impl(const T* d_in, T* d_out, int nx, int ny, int nz, int zb, int ze,
                               int rlo, int rhi, const StencilDesc<T>& st, int tb, cudaStream_t s) {
-  if (tb < 2 || st.order != 1 || std::is_same<T, long long>::value) return cudaErrorNotSupported;
+  if (tb < 2 || st.order < 1 || st.order > 2 || std::is_same<T, long long>::value)
+    return cudaErrorNotSupported;
   const std::vector<T> coef = dense3d_coef(st);
-  const Shape3D sh = classify3d(st.taps, 1);
-  if (sh == Shape3D::star && star3d_enabled())
-    return star3d_tb<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s);
+  const Shape3D sh = classify3d(st.taps, st.order);
+  if (pipe3d_enabled()) {
+    if (st.order == 2)
+      return sh == Shape3D::star
+                 ? pipe3d_star2<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s)
+                 : cudaErrorNotSupported;
+    return sh == Shape3D::star
+               ? pipe3d_star1<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s)
+               : pipe3d_box<T>(sh == Shape3D::poisson, d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi,
+                               coef.data(), tb, s);
+  }
+  if (st.order != 1) return cudaErrorNotSupported;
   if (tb != 2) return cudaErrorNotSupported;
   switch (sh) {
     case Shape3D::star:

@@ -287,24 +287,29 @@ def test_temporal_blocking_matches_sweeps(cuda_lib, orc, name, dt):
                 assert np.array_equal(got[ring], g[ring])
 
 
-@pytest.mark.parametrize("name", ["3d7pt", "poisson", "3d27pt"])
+@pytest.mark.parametrize("name,tbs", [("3d7pt", (2, 3, 4)), ("3d13pt", (2,)), ("poisson", (2,)),
+                                      ("3d27pt", (2,))])
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
-def test_stencil3d_tb2_bit_identical_to_two_sweeps(cuda_lib, orc, name, dt):
-    """Temporal blocking (engine3d_tb.cuh): two fused sweeps == two single sweeps,
+def test_stencil3d_tb_bit_identical_to_single_sweeps(cuda_lib, orc, name, tbs, dt):
+    """Temporal blocking (engine3d_pipe.cuh): Tb fused sweeps == Tb single sweeps,
     bit for bit, and == the oracle within tolerance; odd shapes and z-segments."""
     import torch
     from paper_1907_06154_b200 import device as dev
     st = cuda_lib.convert_stencil(cuda_lib.make_benchmark_stencil(name), dt)
-    for (nx, ny, nz) in ((132, 70, 37), (256, 97, 80)):
+    offs = [t.offset for t in st.taps]
+    cf = np.asarray([t.coeff for t in st.taps], dt)
+    tol = 1e-5 if dt == np.float32 else 1e-12
+    for (nx, ny, nz) in ((132, 70, 37), (256, 97, 80), (64, 11, 9)):
         g = orc.random_grid((nz, ny, nx), dt, 21)
-        a = torch.from_numpy(g).cuda()
-        b, c, f = a.clone(), a.clone(), a.clone()
-        dev.stencil3d_sweep(a, b, st)
-        dev.stencil3d_sweep(b, c, st)
-        dev.stencil3d_tb(a, f, st, 2)
-        assert torch.equal(f, c), (name, nx, ny, nz)
-        offs = [t.offset for t in st.taps]
-        cf = np.asarray([t.coeff for t in st.taps], dt)
-        want = orc.stencil3d(g, offs, cf, st.order, 2)
-        tol = 1e-5 if dt == np.float32 else 1e-12
-        assert max_rel_err(f.cpu().numpy(), want) <= tol
+        for tb in tbs:
+            a = torch.from_numpy(g).cuda()
+            cur = a
+            for _ in range(tb):
+                nxt = cur.clone()
+                dev.stencil3d_sweep(cur, nxt, st)
+                cur = nxt
+            f = a.clone()
+            dev.stencil3d_tb(a, f, st, tb)
+            assert torch.equal(f, cur), (name, tb, nx, ny, nz)
+            want = orc.stencil3d(g, offs, cf, st.order, tb)
+            assert max_rel_err(f.cpu().numpy(), want) <= tol, (name, tb, nx, ny, nz)

@@ -1,11 +1,13 @@
-"""Star pipeline (engine3d_star.cuh) check + timing on one GPU.
+"""3D pipeline engine (engine3d_pipe.cuh) check + timing on one GPU.
 
-  python tools/star_check.py [check] [time]
+  python tools/pipe_check.py [check] [time] [quick] [shapes]
 
-check: TB = 2/3/4 fused launches == TB single sweeps bit for bit, == the
-oracle within tolerance, on odd shapes; unaligned grids (direct kernel).
+check: fused launches == TB single sweeps bit for bit, == the oracle within
+tolerance, on odd shapes, for every shape and compiled depth; unaligned
+grids (direct kernel) through stencil3d_run.
 time: 2048^2 x 514 f32 (headline slab) single sweep and TB = 2/3/4, 512^3
 f32/f64 x20 through stencil3d_run, in GCells/s (cell-updates, interior).
+shapes: 512^3 f32/f64 of 3d13pt / 3d27pt / poisson at TB = 1, 2 and run x20.
 """
 import os
 import sys
@@ -19,16 +21,23 @@ from paper_1907_06154_b200 import device as dev
 from oracle import Oracle, max_rel_err
 
 
+TBS = {"3d7pt": (2, 3, 4), "3d13pt": (2,), "3d27pt": (2,), "poisson": (2,)}
+
+
 def check():
     orc = Oracle()
     bad = 0
-    for dt, tol in ((np.float32, 1e-5), (np.float64, 1e-12)):
-        st = ssam.convert_stencil(ssam.make_benchmark_stencil("3d7pt"), dt)
+    for (dt, tol), name in [(d, n) for d in ((np.float32, 1e-5), (np.float64, 1e-12))
+                            for n in TBS]:
+        st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), dt)
         offs = [t.offset for t in st.taps]
         cf = np.asarray([t.coeff for t in st.taps], dt)
-        for (nx, ny, nz) in ((132, 70, 37), (256, 97, 80), (64, 19, 9), (520, 40, 150), (16, 3, 3)):
+        k = st.order
+        for (nx, ny, nz) in ((132, 70, 37), (256, 97, 80), (64, 19, 9), (520, 40, 150), (16, 5, 5)):
+            if min(nx, ny, nz) < 2 * k + 1:
+                continue
             g = orc.random_grid((nz, ny, nx), dt, 21)
-            for tb in (2, 3, 4):
+            for tb in TBS[name]:
                 a = torch.from_numpy(g).cuda()
                 singles = [a]
                 for _ in range(tb):
@@ -42,17 +51,17 @@ def check():
                 e = max_rel_err(f.cpu().numpy(), want)
                 ok = same and e <= tol
                 bad += not ok
-                print(f"{np.dtype(dt).name} {nx}x{ny}x{nz} tb={tb}: bit-identical={same} "
+                print(f"{name} {np.dtype(dt).name} {nx}x{ny}x{nz} tb={tb}: bit-identical={same} "
                       f"max_rel={e:.3g} {'ok' if ok else 'FAIL'}", flush=True)
         # unaligned width -> direct kernel, and run3d (mixed fused/single)
         for (nx, ny, nz, iters) in ((131, 33, 21, 3), (128, 64, 40, 7), (130, 17, 30, 5)):
             g = orc.random_grid((nz, ny, nx), dt, 5)
-            got = ssam.stencil3d(g, st, ssam.KernelConfig(p=2), iters)
+            got = ssam.stencil3d(g, st, ssam.KernelConfig(p=2, b=max(128, 32 * (2 * k + 1))), iters)
             want = orc.stencil3d(g, offs, cf, st.order, iters)
             e = max_rel_err(got, want)
             ok = e <= tol
             bad += not ok
-            print(f"{np.dtype(dt).name} run {nx}x{ny}x{nz} x{iters}: max_rel={e:.3g} "
+            print(f"{name} {np.dtype(dt).name} run {nx}x{ny}x{nz} x{iters}: max_rel={e:.3g} "
                   f"{'ok' if ok else 'FAIL'}", flush=True)
     print("CHECK", "FAIL" if bad else "OK", bad)
 
@@ -137,6 +146,32 @@ def quick():
     print(os.environ.get("SSAM_B200_LIB", "main"), " ".join(out), flush=True)
 
 
+def shapes():
+    """512^3 single sweeps / TB = 2 / stencil3d_run x20 of the heavier shapes."""
+    n = 512
+    for tdt, npdt in ((torch.float32, np.float32), (torch.float64, np.float64)):
+        a = torch.empty((n, n, n), dtype=tdt, device="cuda")
+        dev.fill_random(a, 0)
+        b = a.clone()
+        for name in ("3d7pt", "3d13pt", "3d27pt", "poisson"):
+            st = ssam.convert_stencil(ssam.make_benchmark_stencil(name), npdt)
+            k = st.order
+            cells = (n - 2 * k) ** 3
+            line = [f"{name} {np.dtype(npdt).name}"]
+            ms = timed(lambda: dev.stencil3d_sweep(a, b, st), 10)
+            line.append(f"tb1={cells / ms / 1e6:.0f}")
+            try:
+                ms = timed(lambda: dev.stencil3d_tb(a, b, st, 2), 10)
+                line.append(f"tb2={2 * cells / ms / 1e6:.0f}")
+            except Exception as ex:  # no fused kernel for this shape
+                line.append(f"tb2=n/a")
+            ms = timed(lambda: dev.stencil3d_run(a, b, st, 20), 2)
+            line.append(f"run20={n ** 3 * 20 / ms / 1e6:.0f} (tb={dev.stencil3d_tb_max(st, npdt)})")
+            print(os.environ.get("SSAM_B200_PIPE", "pipe"), " ".join(line), flush=True)
+        del a, b
+        torch.cuda.empty_cache()
+
+
 if __name__ == "__main__":
     what = sys.argv[1:] or ["check", "time"]
     if "check" in what:
@@ -145,3 +180,5 @@ if __name__ == "__main__":
         time_all()
     if "quick" in what:
         quick()
+    if "shapes" in what:
+        shapes()
