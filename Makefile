@@ -16,7 +16,7 @@ CXXFLAGS := -std=c++17 -O2 -fPIC -Wall -Iinclude -I$(SRC) -I$(CUDA_HOME)/include
 
 CU_SRCS := $(wildcard $(SRC)/*.cu)
 CU_OBJS := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
-CPP_OBJS := $(BUILD)/abi.o $(BUILD)/tmap.o $(BUILD)/grid_io.o
+CPP_OBJS := $(BUILD)/abi.o $(BUILD)/tmap.o $(BUILD)/grid_io.o $(BUILD)/multi.o
 HDRS := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp) include/ssam_b200.h
 
 all: $(LIB) $(CLI) oracle dropin
@@ -96,3 +96,7 @@ dropin:
 endif
 
 .PHONY: dropin
+
+$(BUILD)/multi.o: $(SRC)/multi.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) $(CXXFLAGS) -c $< -o $@

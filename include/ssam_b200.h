@@ -117,6 +117,27 @@ int ssam_b200_stencil3d(int dtype, const void* in, int nx, int ny, int nz, const
                         const ssam_kernel_config* cfg, int iters, void* out,
                         ssam_op_counters* counters);
 
+/* Multi-GPU from one process (the drop-in's device-set variant of
+ * kernels.hpp:231 / :283).  The grid is cut into `ndev` slabs along its
+ * slowest axis (rows in 2D, z-planes in 3D); slab g runs on CUDA device
+ * devices[g] (repeats allowed: two slabs may share a device) with k*Tb ghost
+ * planes on every face shared with a neighbour.  After each fused launch of
+ * Tb sweeps the boundary planes go to the neighbours' ghost planes by
+ * cudaMemcpyPeerAsync (NVLink P2P, peer access enabled on demand), on a copy
+ * stream overlapped with the interior launch.  Results are bit-identical to
+ * ssam_b200_stencil2d / ssam_b200_stencil3d; errors and counters are
+ * theirs, plus SSAM_ERR_INVALID_ARGUMENT for an empty list or a device index
+ * out of range.  *used (optional) receives the number of slabs actually run
+ * (fewer than ndev when a slab would own fewer than k*Tb planes). */
+int ssam_b200_stencil2d_multi(int dtype, const void* in, int width, int height,
+                              const ssam_stencil* st, const ssam_kernel_config* cfg, int iters,
+                              const int* devices, int ndev, void* out, ssam_op_counters* counters,
+                              int* used);
+int ssam_b200_stencil3d_multi(int dtype, const void* in, int nx, int ny, int nz,
+                              const ssam_stencil* st, const ssam_kernel_config* cfg, int iters,
+                              const int* devices, int ndev, void* out, ssam_op_counters* counters,
+                              int* used);
+
 /* A batch of independent grids (same shape and stencil) through the engine
  * with the PCIe copies overlapped: grid k's host->device copy, sweeps and
  * device->host copy run on three streams while neighbouring grids are in

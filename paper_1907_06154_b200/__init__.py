@@ -107,6 +107,10 @@ _sig("ssam_b200_launch_count", [], C.c_uint64)
 _sig("ssam_b200_conv2d", [_i, _p, _i, _i, _p, _i, _i, _PC, _p, _PK])
 _sig("ssam_b200_stencil2d", [_i, _p, _i, _i, _PS, _PC, _i, _p, _PK])
 _sig("ssam_b200_stencil3d", [_i, _p, _i, _i, _i, _PS, _PC, _i, _p, _PK])
+_sig("ssam_b200_stencil2d_multi", [_i, _p, _i, _i, _PS, _PC, _i, C.POINTER(_i), _i, _p, _PK,
+                                   C.POINTER(_i)])
+_sig("ssam_b200_stencil3d_multi", [_i, _p, _i, _i, _i, _PS, _PC, _i, C.POINTER(_i), _i, _p, _PK,
+                                   C.POINTER(_i)])
 _sig("ssam_b200_check_conv2d", [_i, _i, _i, _i, _PC])
 _sig("ssam_b200_check_stencil2d", [_i, _i, _PS, _PC, _i])
 _sig("ssam_b200_check_stencil3d", [_i, _i, _i, _PS, _PC, _i])
@@ -169,6 +173,7 @@ lib = _lib  # raw handle for device-level callers (bench.py, tests)
 EXPORTED = [
     "ssam_b200_abi_version", "ssam_b200_last_error", "ssam_b200_device_count",
     "ssam_b200_default_config", "ssam_b200_launch_count", "ssam_b200_conv2d",
+    "ssam_b200_stencil2d_multi", "ssam_b200_stencil3d_multi",
     "ssam_b200_stencil2d", "ssam_b200_stencil3d", "ssam_b200_check_conv2d",
     "ssam_b200_check_stencil2d", "ssam_b200_check_stencil3d", "ssam_b200_counters_conv2d",
     "ssam_b200_counters_stencil2d", "ssam_b200_counters_stencil3d", "ssam_b200_benchmark_count",
@@ -440,6 +445,37 @@ def stencil3d(grid: np.ndarray, st: Stencil, cfg: Optional[KernelConfig] = None,
     if counters is not None:
         counters._store(cnt)
     return out
+
+
+def stencil_multi(grid: np.ndarray, st: Stencil, devices: Sequence[int],
+                  cfg: Optional[KernelConfig] = None, iters: int = 1,
+                  counters: Optional[OpCounters] = None):
+    """ssam::stencil2d / stencil3d on several GPUs from this process
+    (ssam_b200_stencil2d_multi / _3d_multi): slabs along the slowest axis,
+    slab g on devices[g] (repeats allowed), halos by peer copies.  Returns
+    (result, slabs actually used); the result equals stencil2d/3d bit for bit."""
+    g = _grid(grid, st.dims)
+    if cfg is None:
+        cfg = KernelConfig() if st.dims == 2 else KernelConfig(p=2, b=max(128, 32 * (2 * st.order + 1)))
+    sa = _StencilArgs(st, g.dtype)
+    out = np.empty_like(g)
+    devs = (_i * len(devices))(*devices)
+    used = _i(0)
+    cnt = counters._load() if counters is not None else None
+    pk = C.byref(cnt) if cnt is not None else None
+    if st.dims == 2:
+        s = _lib.ssam_b200_stencil2d_multi(_DT[g.dtype], g.ctypes.data, g.shape[1], g.shape[0],
+                                           sa.ref, C.byref(cfg._c()), iters, devs, len(devices),
+                                           out.ctypes.data, pk, C.byref(used))
+    else:
+        nz, ny, nx = g.shape
+        s = _lib.ssam_b200_stencil3d_multi(_DT[g.dtype], g.ctypes.data, nx, ny, nz, sa.ref,
+                                           C.byref(cfg._c()), iters, devs, len(devices),
+                                           out.ctypes.data, pk, C.byref(used))
+    _raise(s)
+    if counters is not None:
+        counters._store(cnt)
+    return out, used.value
 
 
 def stencil_batch(grids, outs, st: Stencil, iters: int, depth: int = 0) -> None:

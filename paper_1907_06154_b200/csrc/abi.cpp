@@ -510,6 +510,37 @@ template <class T> struct HostStencil {
   template <class... A> static int run(A... a) { return host_stencil<T>(a...); }
 };
 
+// Multi-device host calls (multi.cpp): same validation and counters as the
+// one-device entry points, the device list checked against the runtime.
+template <class T>
+int host_stencil_multi(const void* in, int nx, int ny, int nz, const ssam_stencil* st, int iters,
+                       const int* devices, int ndev, void* out, int* used) {
+  const StencilDesc<T> d = make_desc<T>(st);
+  const int dtype = sizeof(T) == 4 ? SSAM_DTYPE_F32 : (std::is_same<T, double>::value ? 1 : 2);
+  const int tb = st->dims == 2 ? default_tb(dtype, st)
+                               : stencil3d_tb_max(dtype, d.order, classify3d(d.taps, d.order));
+  const cudaError_t e = multi_stencil<T>(static_cast<const T*>(in), static_cast<T*>(out), nx, ny,
+                                         st->dims == 2 ? 1 : nz, d, iters, tb, devices, ndev, used);
+  if (e != cudaSuccess) return cuda_fail(e, "stencil multi");
+  return SSAM_OK;
+}
+template <class T> struct HostStencilMulti {
+  template <class... A> static int run(A... a) { return host_stencil_multi<T>(a...); }
+};
+
+int check_devices(const int* devices, int ndev) {
+  if (!devices || ndev < 1) return fail(SSAM_ERR_INVALID_ARGUMENT, "multi: empty device list");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    count = 0;
+  }
+  for (int i = 0; i < ndev; ++i)
+    if (devices[i] < 0 || devices[i] >= count)
+      return fail(SSAM_ERR_INVALID_ARGUMENT, "multi: device index out of range");
+  return SSAM_OK;
+}
+
 // ---- 1D: conv1d / scan (kernels.hpp:390-447) -----------------------------------
 bool pow2_lanes(int s) { return s >= 2 && s <= 64 && (s & (s - 1)) == 0; }
 
@@ -885,6 +916,39 @@ int ssam_b200_stencil3d(int dtype, const void* in, int nx, int ny, int nz, const
   if (!in || !out) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d: null pointer");
   if (int s = device_ready()) return s;
   if (int s = by_dtype<HostStencil>(dtype, in, nx, ny, nz, st, iters, out)) return s;
+  if (counters) counters_stencil3d(nx, ny, nz, st, c, iters, counters);
+  return SSAM_OK;
+}
+
+int ssam_b200_stencil2d_multi(int dtype, const void* in, int w, int h, const ssam_stencil* st,
+                              const ssam_kernel_config* cfg, int iters, const int* devices,
+                              int ndev, void* out, ssam_op_counters* counters, int* used) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  const ssam_kernel_config c = cfg_or_default(cfg);
+  if (int s = check_stencil2d(w, h, st, c, iters)) return s;
+  if (!in || !out) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil2d: null pointer");
+  if (int s = device_ready()) return s;
+  if (int s = check_devices(devices, ndev)) return s;
+  if (int s = by_dtype<HostStencilMulti>(dtype, in, w, h, 1, st, iters, devices, ndev, out, used))
+    return s;
+  if (counters) counters_stencil2d(w, h, st, c, iters, counters);
+  return SSAM_OK;
+}
+
+int ssam_b200_stencil3d_multi(int dtype, const void* in, int nx, int ny, int nz,
+                              const ssam_stencil* st, const ssam_kernel_config* cfg, int iters,
+                              const int* devices, int ndev, void* out, ssam_op_counters* counters,
+                              int* used) {
+  g_err.clear();
+  if (!dtype_ok(dtype)) return fail(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
+  const ssam_kernel_config c = cfg_or_default(cfg);
+  if (int s = check_stencil3d(nx, ny, nz, st, c, iters)) return s;
+  if (!in || !out) return fail(SSAM_ERR_INVALID_ARGUMENT, "stencil3d: null pointer");
+  if (int s = device_ready()) return s;
+  if (int s = check_devices(devices, ndev)) return s;
+  if (int s = by_dtype<HostStencilMulti>(dtype, in, nx, ny, nz, st, iters, devices, ndev, out, used))
+    return s;
   if (counters) counters_stencil3d(nx, ny, nz, st, c, iters, counters);
   return SSAM_OK;
 }

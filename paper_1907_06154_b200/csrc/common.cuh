@@ -37,6 +37,22 @@ __device__ __forceinline__ float fma_t<float>(float a, float b, float c) { retur
 template <>
 __device__ __forceinline__ double fma_t<double>(double a, double b, double c) { return __fma_rn(a, b, c); }
 
+// Explicitly rounded multiply / add: never contracted into an FMA, so a
+// chain written with mul_t / fma_t / add_t has ONE rounding sequence in
+// every kernel that uses it (bit-identical results across engines).
+template <class T>
+__device__ __forceinline__ T mul_t(T a, T b) { return a * b; }
+template <>
+__device__ __forceinline__ float mul_t<float>(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_t<double>(double a, double b) { return __dmul_rn(a, b); }
+template <class T>
+__device__ __forceinline__ T add_t(T a, T b) { return a + b; }
+template <>
+__device__ __forceinline__ float add_t<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_t<double>(double a, double b) { return __dadd_rn(a, b); }
+
 template <class T>
 __device__ __forceinline__ T shfl_up(T v, int d) { return __shfl_up_sync(kFull, v, d); }
 
@@ -102,8 +118,8 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 
 // Orders this thread's prior generic-proxy shared accesses (and those made
-// visible to it, e.g. by __syncwarp) before its subsequent async-proxy ops:
-// the WAR hand-off when a consumed slot is refilled by TMA.
+// visible to it by an acquiring mbarrier wait) before its subsequent
+// async-proxy ops: the WAR hand-off when a consumed slot is refilled by TMA.
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -184,31 +200,13 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
-// Block until the shared-memory loads that produced rows[..] have returned
-// data.  A ring slot may only be handed back to the TMA unit once its reads
-// are PERFORMED -- issued is not enough: an LDS queued behind MIO traffic can
-// otherwise be overtaken by the refill (observed as whole corrupted boxes).
-// One register of every 16-byte chunk feeds an XOR chain whose result is
-// stored (volatile, to a per-lane scratch word): in-order issue then keeps
-// every later instruction -- the __syncwarp and the refill -- behind the
-// returned data.  Cheaper than fence.proxy.async (a MEMBAR) per box.
-template <class T, int Q, int N>
-__device__ __forceinline__ void wait_loaded(const T (&rows)[N][Q], int first, int count,
-                                            uint32_t scratch) {
-  constexpr int V = 16 / sizeof(T);
-  uint32_t dep = 0;
-#pragma unroll
-  for (int r = 0; r < N; ++r) {
-    if (r < first || r >= first + count) continue;
-#pragma unroll
-    for (int c = 0; c < Q / V; ++c) {
-      uint32_t bits;
-      memcpy(&bits, &rows[r][c * V], sizeof(bits));
-      dep ^= bits;
-    }
-  }
-  asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(scratch), "r"(dep) : "memory");
-}
+// TMA ring protocol used by every engine (the PTX memory-model pattern of a
+// producer/consumer mbarrier pipeline): a consumer lane reads a slot with
+// LDS, then arrives on the slot's EMPTY barrier (mbarrier.arrive has release
+// semantics); the issuing lane waits on it (try_wait has acquire
+// semantics), executes fence.proxy.async (generic-proxy reads ordered
+// before the async-proxy writes of the refill) and only then issues the
+// TMA copy into the slot.
 
 // Q-vector shared load / global store as 16-byte chunks (Q*sizeof(T) in {16, 32}).
 template <class T, int Q>

@@ -77,6 +77,63 @@ template <int K>
 struct StarMask2D {
   __host__ __device__ static constexpr bool has(int j, int t) { return j == K || t == K; }
 };
+template <class Mask> struct IsStar2D { static constexpr bool value = false; };
+template <int K> struct IsStar2D<StarMask2D<K>> { static constexpr bool value = true; };
+
+// One output row of an order-K star as ONE chain per output -- the
+// reference simulator's stage order (kernels.hpp:111-159: taps bucketed by
+// column, rows ascending, one MAD per tap into the shifted partial sum):
+//   left  chain  j = 0..K      (dx = -K..0) flows up:   first tap rounded
+//                               product, then shift + FMA per tap;
+//   right chain  j = 2K..K+1   (dx = K..1) flows down the same way;
+//   out = left + right          (one rounded add).
+// Window row t (dy = t - K) is buf[(rot + t) % NB]; coef(j, t) returns the
+// tap's coefficient.  Written with mul_t / fma_t / add_t only (no
+// contraction freedom), so the single-sweep engines and every temporal-
+// blocking stage produce bit-identical rows.
+template <class T, int Q, int K, int NB, class CF>
+__device__ __forceinline__ void star_row_chain(const T (&buf)[NB][Q], int rot, CF coef,
+                                               T (&acc)[Q]) {
+  constexpr int NR = 2 * K + 1;
+  {
+    const T c = coef(0, K);
+    const int b = (rot + K) % NB;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = mul_t(c, buf[b][q]);
+  }
+#pragma unroll
+  for (int j = 1; j <= K; ++j) {
+    shift_up1<T, Q>(acc);
+#pragma unroll
+    for (int t = 0; t < NR; ++t) {
+      if (!StarMask2D<K>::has(j, t)) continue;
+      const T c = coef(j, t);
+      const int b = (rot + t) % NB;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) acc[q] = fma_t(c, buf[b][q], acc[q]);
+    }
+  }
+  if constexpr (K > 0) {
+    T accr[Q];
+    {
+      const T c = coef(NR - 1, K);
+      const int b = (rot + K) % NB;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) accr[q] = mul_t(c, buf[b][q]);
+    }
+#pragma unroll
+    for (int j = NR - 2; j > K; --j) {
+      shift_down1<T, Q>(accr);
+      const T c = coef(j, K);  // off-centre columns of a star: the centre row only
+      const int b = (rot + K) % NB;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) accr[q] = fma_t(c, buf[b][q], accr[q]);
+    }
+    shift_down1<T, Q>(accr);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) acc[q] = add_t(acc[q], accr[q]);
+  }
+}
 
 // Column partial of filter column j: window row t is buf[(rot + t) % NB].
 template <class T, int Q, int NR, class Mask, int NB, int CAP>
@@ -101,6 +158,11 @@ __device__ __forceinline__ bool colpart_ct(const T (&buf)[NB][Q], int rot, int j
 template <class T, int Q, int NR, int MC, class Mask, int NB, int CAP>
 __device__ __forceinline__ void ssam_row_ct(const T (&buf)[NB][Q], int rot,
                                             const Ssam2DParams<T, CAP>& p, T (&acc)[Q]) {
+  if constexpr (IsStar2D<Mask>::value && MC == NR) {
+    star_row_chain<T, Q, (NR - 1) / 2, NB>(buf, rot,
+                                           [&](int j, int t) { return p.coef[j * NR + t]; }, acc);
+    return;
+  }
   constexpr int R = (MC - 1) / 2, L = MC - 1 - R;
   // left chain: columns j = 0..L flow up into the centre lane
 #pragma unroll
@@ -227,8 +289,8 @@ __device__ __forceinline__ void store_row(const Ssam2DParams<T, CAP>& p, const S
     if (sp.x0 + q >= sp.xlo && sp.x0 + q < sp.xhi) row[q] = acc[q];
 }
 
-// Shared memory of the TMA kernel: per warp D boxes of RB rows, D mbarriers
-// and a 32-word scratch line for wait_loaded().
+// Shared memory of the TMA kernel: per warp D boxes of RB rows, D full
+// mbarriers and a 128-byte line holding the D empty mbarriers (D <= 16).
 template <class T, int Q, int RB, int D>
 __host__ __device__ constexpr size_t tma2d_smem(int warps) {
   return static_cast<size_t>(warps) *
@@ -257,13 +319,16 @@ __global__ void __launch_bounds__(128)
   uint64_t* bars = reinterpret_cast<uint64_t*>(
                        smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * BOX_BYTES) +
                    wib * D;
-  const uint32_t scratch =
-      smem_u32(smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * (BOX_BYTES + 8)) +
-      (wib * 32 + lane) * 4;
+  static_assert(D <= 16, "empty barriers fit the warp's 128-byte line");
+  uint64_t* empty = reinterpret_cast<uint64_t*>(
+      smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * (BOX_BYTES + 8) + wib * 128);
   if (lane == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
-    for (int s = 0; s < D; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < D; ++s) {
+      mbar_init(smem_u32(&bars[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 32);
+    }
     fence_mbar_init();
   }
   __syncwarp();
@@ -279,6 +344,19 @@ __global__ void __launch_bounds__(128)
   };
   if (lane == 0)
     for (int j = 0; j < min(D, nbox); ++j) issue(j);
+  // Ring hand-back (PTX memory model): every lane arrives (release) on the
+  // slot's empty barrier after its last read of box j; lane 0 waits
+  // (acquire), fences generic -> async proxy, and refills the slot with
+  // box j + D.
+  auto recycle = [&](int j) {
+    const int s = j % D;
+    mbar_arrive(smem_u32(&empty[s]));
+    if (lane == 0 && j + D < nbox) {
+      mbar_wait(smem_u32(&empty[s]), (j / D) & 1);
+      fence_proxy_async();
+      issue(j + D);
+    }
+  };
 
   if constexpr (RB == NR) {
     // Whole-window boxes: box j's NR rows are read into one half of a
@@ -292,9 +370,7 @@ __global__ void __launch_bounds__(128)
       const T* slot = ring + s * RB * ROW + Q * lane;
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) lds_q<T, Q>(slot + rr * ROW, win[cur + rr]);
-      wait_loaded<T, Q, 2 * NR>(win, cur, NR, scratch);
-      __syncwarp();  // every lane has read slot s before it is refilled
-      if (lane == 0 && j + D < nbox) issue(j + D);
+      recycle(j);  // slot s is in registers: refill it while the rows compute
 #pragma unroll
       for (int rr = 0; rr < NR; ++rr) {
         const int i = j * NR + rr;
@@ -315,8 +391,8 @@ __global__ void __launch_bounds__(128)
   } else {
     // Tall windows: the window shifts down one row per step and exactly one
     // row body is emitted (a large filter's row is thousands of FMAs; more
-    // unrolling only thrashes the instruction cache).  A slot is refilled
-    // after its last row was consumed by arithmetic, so its LDS are done.
+    // unrolling only thrashes the instruction cache).  A slot is handed back
+    // after its last row was read.
     T win[NR][Q];
     for (int j = 0; j < nbox; ++j) {
       const int s = j % D;
@@ -335,12 +411,9 @@ __global__ void __launch_bounds__(128)
           T acc[Q];
           ssam_row<T, Q, NR, MC, Mask, NR, CAP>(win, 0, p, acc);
           store_row<T, Q, CAP>(p, sp, y0 + i - (NR - 1), acc);
-        } else {
-          wait_loaded<T, Q, NR>(win, NR - 1, 1, scratch);
         }
       }
-      __syncwarp();
-      if (lane == 0 && j + D < nbox) issue(j + D);
+      recycle(j);
     }
   }
 }

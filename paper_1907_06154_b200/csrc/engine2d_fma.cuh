@@ -38,7 +38,8 @@
 // Rows arrive as RB-row TMA boxes (zero fill = zero boundary) in a per-warp
 // ring of D slots.  A box is handed back once its rows have fed a pass's
 // FFMAs (so its LDS have returned); in the prologue, where the window is
-// taller than the ring, as soon as its rows have returned (wait_loaded).
+// taller than the ring, as soon as its rows were read (every lane arrives
+// on the slot's empty barrier; lane 0 acquires it before the refill).
 #pragma once
 
 #include "engine2d.cuh"
@@ -122,8 +123,9 @@ __global__ void __launch_bounds__(128)
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(nwarps) * D * SLOT_BYTES) +
       wib * D;
-  const uint32_t scratch =
-      smem_u32(smem_raw + static_cast<size_t>(nwarps) * D * (SLOT_BYTES + 8)) + threadIdx.x * 4;
+  static_assert(D <= 16, "empty barriers fit the warp's 128-byte line");
+  uint64_t* empty = reinterpret_cast<uint64_t*>(
+      smem_raw + static_cast<size_t>(nwarps) * D * (SLOT_BYTES + 8) + wib * 128);
   T* scoef = reinterpret_cast<T*>(smem_raw +
                                   static_cast<size_t>(nwarps) * (D * (SLOT_BYTES + 8) + 128));
   if constexpr (!UNROLL) {
@@ -157,7 +159,10 @@ __global__ void __launch_bounds__(128)
   if (lane == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
-    for (int s = 0; s < D; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < D; ++s) {
+      mbar_init(smem_u32(&bars[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 32);
+    }
     fence_mbar_init();
   }
   __syncwarp();
@@ -174,6 +179,17 @@ __global__ void __launch_bounds__(128)
   };
   if (lane == 0)
     for (int b = 0; b < min(D, nbox); ++b) issue(b);
+  // Ring hand-back (PTX memory model): every lane arrives (release) on box
+  // b's empty barrier after its last read of it; lane 0 waits (acquire),
+  // fences generic -> async proxy and refills the slot with box b + D.
+  auto recycle = [&](int b) {
+    mbar_arrive(smem_u32(&empty[b % D]));
+    if (lane == 0 && b + D < nbox) {
+      mbar_wait(smem_u32(&empty[b % D]), (b / D) & 1);
+      fence_proxy_async();
+      issue(b + D);
+    }
+  };
   auto row_ptr = [&](int s) -> const T* {
     const int b = s / RB;
     return ring + (b % D) * SLOT + (s - b * RB) * ROW + dmis + Q * lane;
@@ -235,11 +251,7 @@ __global__ void __launch_bounds__(128)
     const int s = OFF + t;
     if (t == 0 || s % RB == 0) wait_box(s / RB);
     lds_row(row_ptr(s), win[t]);
-    if (!STARX && (s + 1) % RB == 0) {  // box s/RB fully read: hand it back once returned
-      wait_loaded<T, Q, NW>(win, max(0, t + 1 - RB), min(RB, t + 1), scratch);
-      __syncwarp();
-      if (lane == 0 && s / RB + D < nbox) issue(s / RB + D);
-    }
+    if (!STARX && (s + 1) % RB == 0) recycle(s / RB);  // box s/RB fully read
   }
 
   T* outp = p.out + static_cast<size_t>(y0) * p.W + x0;
@@ -419,15 +431,9 @@ __global__ void __launch_bounds__(128)
     }
     if constexpr (STARX) {
       // centre rows below s + RY - SK are done: boxes wholly below are free
-      __syncwarp();
-      while ((rel + 1) * RB <= s + RY - SK) {
-        if (lane == 0 && rel + D < nbox) issue(rel + D);
-        ++rel;
-      }
+      while ((rel + 1) * RB <= s + RY - SK) recycle(rel++);
     } else if ((s + RY) % RB == 0) {
-      // the pass's rows have fed its FFMAs: a box whose last row this was is free
-      __syncwarp();
-      if (lane == 0 && s / RB + D < nbox) issue(s / RB + D);
+      recycle(s / RB);  // the pass read the last row of box s/RB
     }
     if constexpr (STARX) {
       cw += RY;

@@ -116,8 +116,8 @@ __host__ __device__ constexpr size_t box_slot_elems(int brows, int bcols) {
 }
 
 // Shared memory of the TMA kernel: DZ plane boxes shared by the CTA's warps
-// (sx strips x sy row groups), a full and an empty mbarrier per slot, and
-// the wait_loaded() scratch line.
+// (sx strips x sy row groups), a full and an empty mbarrier per slot (the
+// empty barrier counts one arrive per consumer lane), and 128 B per warp.
 template <class T, int Q, int RY, int K, int DZ>
 __host__ __device__ constexpr size_t ring3d_bytes(int sx, int sy, int v) {
   return static_cast<size_t>(DZ) *
@@ -382,13 +382,12 @@ __global__ void __launch_bounds__(256)
   T* ring = reinterpret_cast<T*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + DZ * slot_elems * sizeof(T));
   uint64_t* empty = full + DZ;
-  const uint32_t scratch = smem_u32(empty + DZ) + threadIdx.x * 4;
   if (threadIdx.x == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
     for (int s = 0; s < DZ; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), wpb);
+      mbar_init(smem_u32(&empty[s]), 32 * wpb);
     }
     fence_mbar_init();
   }
@@ -399,7 +398,10 @@ __global__ void __launch_bounds__(256)
   // flattened (ny*nz)-row view; planes outside [0, nz) land outside -> zeros.
   auto issue = [&](int i) {
     const int s = i % DZ;
-    if (i >= DZ) mbar_wait(smem_u32(&empty[s]), ((i / DZ) - 1) & 1);
+    if (i >= DZ) {
+      mbar_wait(smem_u32(&empty[s]), ((i / DZ) - 1) & 1);  // acquire: every lane's reads done
+      fence_proxy_async();  // generic-proxy reads before the async-proxy refill
+    }
     const uint32_t bar = smem_u32(&full[s]);
     const int z = z0 - K + i;
     const int row = (z >= 0 && z < p.nz) ? z * p.ny + (y_cta0 - K) : -brows;
@@ -415,9 +417,7 @@ __global__ void __launch_bounds__(256)
                     Q * lane;
 #pragma unroll
     for (int r = 0; r < NROW; ++r) lds_q<T, Q>(slot + r * bcols, dst[r]);
-    wait_loaded<T, Q, NROW>(dst, 0, NROW, scratch);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+    mbar_arrive(smem_u32(&empty[s]));  // release: this lane's reads of slot s are done
     if (threadIdx.x == 0 && i >= 1 && i - 1 + DZ < count) issue(i - 1 + DZ);
   };
 
@@ -562,13 +562,12 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
   T* ring = reinterpret_cast<T*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + DZ * slot_elems * sizeof(T));
   uint64_t* empty = full + DZ;
-  const uint32_t scratch = smem_u32(empty + DZ) + threadIdx.x * 4;
   if (threadIdx.x == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
     for (int s = 0; s < DZ; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), wpb);
+      mbar_init(smem_u32(&empty[s]), 32 * wpb);
     }
     fence_mbar_init();
   }
@@ -577,7 +576,10 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
   griddep_launch();  // let the next grid fill SMs as this one drains
   auto issue = [&](int i) {
     const int s = i % DZ;
-    if (i >= DZ) mbar_wait(smem_u32(&empty[s]), ((i / DZ) - 1) & 1);
+    if (i >= DZ) {
+      mbar_wait(smem_u32(&empty[s]), ((i / DZ) - 1) & 1);  // acquire: every lane's reads done
+      fence_proxy_async();  // generic-proxy reads before the async-proxy refill
+    }
     const uint32_t bar = smem_u32(&full[s]);
     const int z = z0 - K + i;
     const int row = (z >= 0 && z < p.nz) ? z * p.ny + (y_cta0 - K) : -brows;
@@ -597,22 +599,13 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
     const T* slot = ring + s * slot_elems + wx * sub_elems + static_cast<size_t>(wy * RY) * BW;
 #pragma unroll
     for (int r = 0; r < NROW; ++r) lds_q<T, Q>(slot + r * BW + VQ + Q * lane, dst[r]);
-    uint32_t dep = 0;
 #pragma unroll
     for (int r = 0; r < NROW; ++r) {
       if (!halo_row_needed<K, Mask, RY>(r)) continue;
 #pragma unroll
-      for (int c = 0; c < K; ++c) {
-        hdst[r][c] = slot[r * BW + hoff0 + hstep * c];
-        uint32_t bits;
-        memcpy(&bits, &hdst[r][c], sizeof(bits));
-        dep ^= bits;
-      }
+      for (int c = 0; c < K; ++c) hdst[r][c] = slot[r * BW + hoff0 + hstep * c];
     }
-    wait_loaded<T, Q, NROW>(dst, 0, NROW, scratch);
-    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(scratch), "r"(dep) : "memory");
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+    mbar_arrive(smem_u32(&empty[s]));  // release: this lane's reads of slot s are done
     if (threadIdx.x == 0 && i >= 1 && i - 1 + DZ < count) issue(i - 1 + DZ);
   };
 

@@ -94,6 +94,16 @@ cudaError_t pipe3d_box(bool poisson, const T* d_in, T* d_out, int nx, int ny, in
 // per shape; SSAM_B200_3D_TB caps it (1 = single sweeps).
 int stencil3d_tb_max(int dtype, int order, Shape3D shape);
 
+// ---- one process, several devices (multi.cpp) --------------------------------
+// Host grid in -> `iters` sweeps on slabs along the slowest axis (rows in 2D,
+// nz = 1; z-planes in 3D), slab g on devices[g] with k*tb ghost planes per
+// shared face, halos by cudaMemcpyPeerAsync overlapped with the interior ->
+// host grid out.  Bit-identical to the one-device run.  *used = the number
+// of slabs (fewer than ndev when a slab would own fewer than k*tb planes).
+template <class T>
+cudaError_t multi_stencil(const T* h_in, T* h_out, int nx, int ny, int nz, const StencilDesc<T>& st,
+                          int iters, int tb, const int* devices, int ndev, int* used);
+
 // ---- direct-gather kernels (generic path: any order / tap set) -------------
 // Bit-faithful to the oracle's summation order (double accumulation for FP,
 // no FMA contraction), used where no SSAM specialisation applies.

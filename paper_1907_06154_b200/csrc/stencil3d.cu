@@ -5,7 +5,7 @@
 // mask: 3d7pt (star K=1), 3d13pt (star K=2), 3d27pt (box K=1), poisson
 // (3x3x3 minus corners); any other tap set of order <= 2 runs the dense
 // engine with zero cells, larger orders the direct-gather kernel.
-#include "engine3d_tb.cuh"
+#include "engine3d.cuh"
 #include "launch.cuh"
 
 namespace ssam_b200 {
@@ -97,12 +97,10 @@ cudaError_t stencil3d_sweep<long long>(const long long* i, long long* o, int nx,
 
 bool stencil3d_peer_fused(int dtype, int order) { return order <= (dtype == 2 ? 1 : 2); }
 
-// ---- temporal blocking (Tb = 2), engine3d_tb.cuh --------------------------------
-// SSAM_B200_3D_TB=1 disables the fused path (plain sweeps).
+// ---- temporal blocking: the pipeline engine (engine3d_pipe.cuh) ---------------
 
-
-// SSAM_B200_PIPE=0 routes every 3D shape back to the generic engines below
-// (engine3d.cuh / engine3d_tb.cuh) for A/B runs.
+// SSAM_B200_PIPE=0 routes single sweeps of every 3D shape back to the
+// generic z-streaming engine (engine3d.cuh) for A/B runs, without fusion.
 bool pipe3d_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("SSAM_B200_PIPE");
@@ -120,77 +118,11 @@ int stencil3d_tb_max(int dtype, int order, Shape3D shape) {
   if (dtype == 2) return 1;
   const bool star1 = order == 1 && shape == Shape3D::star;
   const char* e = std::getenv("SSAM_B200_3D_TB");
-  if (!pipe3d_enabled()) return (star1 && (!e || std::atoi(e) >= 2)) ? 2 : 1;
+  if (!pipe3d_enabled()) return 1;
   const int most = star1 ? 4 : (order == 1 || (order == 2 && shape == Shape3D::star)) ? 2 : 1;
   const bool star2 = order == 2 && shape == Shape3D::star;
   const int want = e ? std::atoi(e) : (star1 || (star2 && dtype == 0) ? 2 : 1);
   return std::max(1, std::min(want, most));
-}
-
-template <class T, class Mask>
-cudaError_t launch_tb3d(const T* d_in, T* d_out, int nx, int ny, int nz, int z_begin, int z_end,
-                        int zr_lo, int zr_hi, const T* coef, cudaStream_t s) {
-  // stage-2 rows per warp: fp32 4 (RY 3 / 5: 937 / 944 vs 1040 GCells/s at
-  // 2048^2 x 514), fp64 5 (504 vs 461 at 2048^2 x 130, 422 vs 388 at 512^3)
-  constexpr int K = 1, M = 3, Q = Lanes<T>::Q, RY = sizeof(T) == 4 ? 4 : 5, CAP = 27;
-  // 8-warp CTAs for the fp32 star; fp64 and the heavier masks hold ~160
-  // registers and run 4-warp CTAs (three resident per SM instead of one).
-#ifndef SSAM_TB3_SY32
-#define SSAM_TB3_SY32 4
-#endif
-  constexpr int SY = (std::is_same<Mask, StarMask3<1>>::value && sizeof(T) == 4) ? SSAM_TB3_SY32 : 2;
-  using G = Tb3Geom<T, Q, K, RY, SY>;
-  constexpr int VQ = 16 / sizeof(T);
-  if (nx % VQ != 0 || !aligned16(d_in) || !aligned16(d_out)) return cudaErrorNotSupported;
-  // outputs [z_begin, z_end) within the global interior [zr_lo, zr_hi); the
-  // fused pair reads planes z_begin-2K .. z_end-1+2K (a slab's ghosts)
-  // (also clamped to the buffer's interior: ring bounds may lie outside it)
-  const int zb = std::max({z_begin, zr_lo, K}), ze = std::min({z_end, zr_hi, nz - K});
-  const int yrows = ny - 2 * K;
-  if (ze <= zb || yrows <= 0 || nx - 2 * K <= 0) return cudaSuccess;
-  Ssam3DTmaParams<T, CAP> P;
-  std::memset(&P, 0, sizeof(P));
-  Ssam3DParams<T, CAP>& p = P.p;
-  apply_peer_halo(p);
-  p.in = d_in;
-  p.out = d_out;
-  p.nx = nx;
-  p.ny = ny;
-  p.nz = nz;
-  const LanePlan lp = plan_lanes(4 * K + 1, Q);  // two sweeps: 2K columns each side
-  p.A = lp.A;
-  p.V = lp.V;
-  p.nstrips = (nx + lp.V - 1) / lp.V;
-  p.ygroups = (yrows + RY - 1) / RY;
-  p.ring = K;
-  p.vec_ok = 1;
-  const int zrows = ze - zb;
-  // Long z-segments amortise the 4-plane prologue of the fused pair (2048^2
-  // x 514: 908 / 991 / 1028 / 1053 GCells/s at 16 / 32 / 64 / 128 planes),
-  // as long as the grid keeps about four waves of CTAs (512^3 wants 32-64).
-  const long long xy_ctas = static_cast<long long>(p.nstrips) * ((yrows + G::ROWS2 - 1) / G::ROWS2);
-  int zseg = std::min(zrows, 128);
-  while (zseg > 16 && xy_ctas * ((zrows + zseg - 1) / zseg) < 4 * 2 * kSMs) zseg /= 2;
-  if (const char* e = std::getenv("SSAM_B200_3D_TB_ZSEG")) zseg = std::max(4, std::atoi(e));
-  p.zseg = zseg;
-  p.z_begin = zb;
-  p.z_end = ze;
-  p.zr_lo = zr_lo;
-  p.zr_hi = zr_hi;
-  p.cta_sx = 1;
-  std::memcpy(p.coef, coef, sizeof(T) * M * M * M);
-  const dim3 grid(p.nstrips, (yrows + G::ROWS2 - 1) / G::ROWS2, (zrows + zseg - 1) / zseg);
-  cudaError_t e = make_tmap_2d(&P.tmap, d_in, sizeof(T), nx, static_cast<uint64_t>(ny) * nz,
-                               sizeof(T) * nx, G::BW, G::BROWS);
-  if (e != cudaSuccess) return e;
-  auto kern = peer_halo_slot() ? ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP, SY, true>
-                                : ssam3d_tb2_kernel<T, Q, K, Mask, RY, CAP, SY, false>;
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
-  if (e != cudaSuccess) return e;
-  e = launch_pdl(kern, grid, dim3(G::THREADS), G::SMEM, s, P);
-  if (e != cudaSuccess) return e;
-  note_launch();
-  return cudaGetLastError();
 }
 
 template <class T>
@@ -200,26 +132,15 @@ cudaError_t stencil3d_tb_impl(const T* d_in, T* d_out, int nx, int ny, int nz, i
     return cudaErrorNotSupported;
   const std::vector<T> coef = dense3d_coef(st);
   const Shape3D sh = classify3d(st.taps, st.order);
-  if (pipe3d_enabled()) {
-    if (st.order == 2)
-      return sh == Shape3D::star
-                 ? pipe3d_star2<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s)
-                 : cudaErrorNotSupported;
+  if (!pipe3d_enabled()) return cudaErrorNotSupported;
+  if (st.order == 2)
     return sh == Shape3D::star
-               ? pipe3d_star1<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s)
-               : pipe3d_box<T>(sh == Shape3D::poisson, d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi,
-                               coef.data(), tb, s);
-  }
-  if (st.order != 1) return cudaErrorNotSupported;
-  if (tb != 2) return cudaErrorNotSupported;
-  switch (sh) {
-    case Shape3D::star:
-      return launch_tb3d<T, StarMask3<1>>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), s);
-    case Shape3D::poisson:
-      return launch_tb3d<T, PoissonMask3>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), s);
-    default:
-      return launch_tb3d<T, DenseMask3>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), s);
-  }
+               ? pipe3d_star2<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s)
+               : cudaErrorNotSupported;
+  return sh == Shape3D::star
+             ? pipe3d_star1<T>(d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi, coef.data(), tb, s)
+             : pipe3d_box<T>(sh == Shape3D::poisson, d_in, d_out, nx, ny, nz, zb, ze, rlo, rhi,
+                             coef.data(), tb, s);
 }
 
 template <>

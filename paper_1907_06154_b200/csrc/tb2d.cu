@@ -39,48 +39,17 @@ struct alignas(64) Tb2DParams {
   T coef[CAP];
 };
 
-// One stage's output row from its NR-row window (bidirectional chain, as in
-// engine2d.cuh); window row t <-> dy = t - K.
-// Window row t lives in register slot (rot + t) % NR (rotation by index,
-// `rot` folds to a constant after unrolling).  Single FMA chain per output:
-// every tap FMAs straight into the shifted partial sum -- the reference
-// simulator's stage order (kernels.hpp:111-159) -- so the 1-tap side columns
-// of a star cost one FFMA, not a column-partial FMUL plus an FADD.
+// One stage's output row from its NR-row window: the single-sweep engines'
+// star chain (engine2d.cuh star_row_chain), so Tb fused sweeps are
+// bit-identical to Tb single sweeps.  Window row t lives in register slot
+// (rot + t) % NR (rotation by index, `rot` folds to a constant after
+// unrolling).
 template <class T, int Q, int K, class Mask, int CAP>
 __device__ __forceinline__ void tb_stage_row(const T (&w)[2 * K + 1][Q], int rot,
                                              const Tb2DParams<T, CAP>& p, T (&acc)[Q]) {
+  static_assert(IsStar2D<Mask>::value, "temporal blocking is compiled for star stencils");
   constexpr int NR = 2 * K + 1;
-  auto colfma = [&](int j, T (&a)[Q]) {
-#pragma unroll
-    for (int t = 0; t < NR; ++t) {
-      if (Mask::has(j, t)) {
-        const T c = p.coef[j * NR + t];
-        const int b = (rot + t) % NR;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) a[q] = fma_t(c, w[b][q], a[q]);
-      }
-    }
-  };
-#pragma unroll
-  for (int q = 0; q < Q; ++q) acc[q] = T(0);
-#pragma unroll
-  for (int j = 0; j <= K; ++j) {
-    if (j > 0) shift_up1<T, Q>(acc);
-    colfma(j, acc);
-  }
-  if constexpr (K > 0) {
-    T accr[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) accr[q] = T(0);
-#pragma unroll
-    for (int j = NR - 1; j > K; --j) {
-      if (j < NR - 1) shift_down1<T, Q>(accr);
-      colfma(j, accr);
-    }
-    shift_down1<T, Q>(accr);
-#pragma unroll
-    for (int q = 0; q < Q; ++q) acc[q] += accr[q];
-  }
+  star_row_chain<T, Q, K, NR>(w, rot, [&](int j, int t) { return p.coef[j * NR + t]; }, acc);
 }
 
 template <class T, int Q, int K, class Mask, int TB, int RB, int D, int CAP>
@@ -110,10 +79,16 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
   uint64_t* bars = reinterpret_cast<uint64_t*>(
                        smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * BOX_BYTES) +
                    wib * D;
+  static_assert(D <= 16, "empty barriers fit the warp's 128-byte line");
+  uint64_t* empty = reinterpret_cast<uint64_t*>(
+      smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * (BOX_BYTES + 8) + wib * 128);
   if (lane == 0) {
     prefetch_tmap(&p.tmap);
 #pragma unroll
-    for (int s = 0; s < D; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    for (int s = 0; s < D; ++s) {
+      mbar_init(smem_u32(&bars[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 32);
+    }
     fence_mbar_init();
   }
   __syncwarp();
@@ -182,8 +157,14 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
         }
       }
     }
-    __syncwarp();  // the box's rows were all consumed by arithmetic above
-    if (lane == 0 && j + D < nbox) issue(j + D);
+    // ring hand-back: every lane releases the slot after its reads, lane 0
+    // acquires, fences generic -> async proxy and refills it
+    mbar_arrive(smem_u32(&empty[s]));
+    if (lane == 0 && j + D < nbox) {
+      mbar_wait(smem_u32(&empty[s]), (j / D) & 1);
+      fence_proxy_async();
+      issue(j + D);
+    }
   }
 }
 
@@ -228,7 +209,7 @@ cudaError_t launch_tb(const T* in, T* out, int W, int H, int yb, int ye, int rlo
   std::memcpy(p.coef, c.data(), sizeof(T) * CAP);
   cudaError_t e = make_tmap_2d(&p.tmap, in, sizeof(T), W, H, sizeof(T) * W, 32 * Q, RB);
   if (e != cudaSuccess) return e;
-  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * D * (RB * 32 * Q * sizeof(T) + 8);
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * (D * (RB * 32 * Q * sizeof(T) + 8) + 128);
   const dim3 grid((p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock, (rows + p.seg - 1) / p.seg);
   e = launch_pdl(tb2d_kernel<T, Q, K, Mask, TB, RB, D, CAP>, grid, dim3(32 * kWarpsPerBlock), smem,
                  s, p);

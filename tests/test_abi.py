@@ -88,3 +88,23 @@ def test_peer_entry_points_refuse_without_device(lib):
     rc = lib.lib.ssam_b200_stencil3d_sweep_peer(0, None, None, 8, 8, 8, 0, 8, sa.ref,
                                                 ctypes.byref(halo), None)
     assert rc != 0 and lib.lib.ssam_b200_last_error()
+
+
+def test_multi_entry_points_validate_before_the_device(lib):
+    """ssam_b200_stencil2d_multi / _3d_multi: the single-device checks come
+    first (same statuses), then the device list; no CPU path."""
+    if lib.device_available():
+        pytest.skip("a device is present; covered by tests/test_gpu_multi.py")
+    st = lib.convert_stencil(lib.make_benchmark_stencil("3d7pt"), np.float32)
+    g = np.zeros((16, 16, 16), np.float32)
+    with pytest.raises(lib.InvalidArgument):
+        lib.stencil_multi(g, st, [0, 1], iters=0)  # iters < 1, as ssam::stencil3d
+    st2 = lib.convert_stencil(lib.make_benchmark_stencil("2d5pt"), np.float32)
+    with pytest.raises(lib.InvalidArgument):
+        lib.stencil_multi(np.zeros((2, 64), np.float32), st2, [0])  # domain < 2k+1
+    with pytest.raises(lib.NoDevice):
+        lib.stencil_multi(g, st, [0, 1])
+    sa = lib._StencilArgs(st, np.float32)
+    rc = lib.lib.ssam_b200_stencil3d_multi(9, None, 8, 8, 8, sa.ref, None, 1, None, 0, None,
+                                           None, None)
+    assert rc == lib.SSAM_ERR_INVALID_ARGUMENT
