@@ -92,6 +92,20 @@ typedef struct {
   const void* coeffs; /* ntaps elements of the call's dtype */
 } ssam_stencil;
 
+/* ssam::LatencyProfile (perf_model.hpp:14-26) measured on this device, in SM
+ * cycles of one warp instruction on a dependent chain; t_l2_read and the SM
+ * clock are extra (see csrc/latency.cu for each micro-benchmark). */
+typedef struct {
+  double t_shfl;
+  double t_mad;
+  double t_smem_read;
+  double t_reg;
+  double t_gmem_read;  /* HBM: coalesced 128-byte lines, random over 256 MiB */
+  double t_gmem_write; /* st.global.wt + fence.acq_rel.gpu */
+  double t_l2_read;    /* same chase over 16 MiB (L2 hits) */
+  double sm_clock_mhz;
+} ssam_latency_profile;
+
 /* ---- library ------------------------------------------------------------ */
 int ssam_b200_abi_version(void);
 /* Message for the last non-OK status on the calling thread ("" if none). */
@@ -116,6 +130,9 @@ int ssam_b200_stencil2d(int dtype, const void* in, int width, int height, const 
 int ssam_b200_stencil3d(int dtype, const void* in, int nx, int ny, int nz, const ssam_stencil* st,
                         const ssam_kernel_config* cfg, int iters, void* out,
                         ssam_op_counters* counters);
+
+/* Runs the latency micro-benchmarks on the current device (a few ms). */
+int ssam_b200_measure_latency(ssam_latency_profile* out);
 
 /* Multi-GPU from one process (the drop-in's device-set variant of
  * kernels.hpp:231 / :283).  The grid is cut into `ndev` slabs along its
@@ -258,6 +275,13 @@ int ssam_b200_ipc_alloc(size_t bytes, void** d_ptr, void* handle);
 int ssam_b200_ipc_free(void* d_ptr);
 int ssam_b200_ipc_open(const void* handle, void** d_ptr);
 int ssam_b200_ipc_close(void* d_ptr);
+/* Device-side generation flags for the peer path (no host barrier per
+ * sweep): write_u32 stores `value` to the 32-bit word at d_addr (local or
+ * IPC-mapped peer memory) once the stream's prior work is done and visible;
+ * wait_u32 holds the stream until the word is >= value.  Both are stream
+ * memory operations (cuStreamWriteValue32 / cuStreamWaitValue32). */
+int ssam_b200_stream_write_u32(void* d_addr, uint32_t value, void* stream);
+int ssam_b200_stream_wait_u32(const void* d_addr, uint32_t value, void* stream);
 
 /* iters sweeps with ping-pong buffers.  d_a holds the input; d_b is scratch
  * of the same size whose ring this call initialises.  *d_result receives

@@ -8,6 +8,7 @@
 //   conv2d     kernels.hpp:189-225  ->  ssam_b200_conv2d
 //   stencil2d  kernels.hpp:231-277  ->  ssam_b200_stencil2d
 //   stencil3d  kernels.hpp:283-384  ->  ssam_b200_stencil3d
+//   (+ device-set overloads of both -> ssam_b200_stencil2d_multi / _3d_multi)
 //
 // The argument types stay the reference's own (Grid2D/Grid3D, Filter2D,
 // Stencil, KernelConfig, OpCounters from ssam/grid.hpp, ssam/filter.hpp,
@@ -151,6 +152,43 @@ Grid3D<T> stencil3d(const Grid3D<T>& in, const Stencil<T>& st, const KernelConfi
   b200_detail::check(ssam_b200_stencil3d(b200_detail::Dtype<T>::value, in.data.data(), in.nx,
                                          in.ny, in.nz, &sa.s, &c, iters, out.data.data(),
                                          counters ? &oc : nullptr));
+  b200_detail::from_c(oc, counters);
+  return out;
+}
+
+// Multi-GPU extensions (not in the reference): the same calls on a device
+// set from one process -- slabs along the slowest axis, slab g on
+// devices[g], halos peer-copied between fused launches
+// (ssam_b200_stencil2d_multi / _3d_multi).  Results are bit-identical to the
+// one-device calls above; errors and counters are theirs.
+template <class T>
+Grid2D<T> stencil2d(const Grid2D<T>& in, const Stencil<T>& st, const KernelConfig& cfg,
+                    int iters, const std::vector<int>& devices, OpCounters* counters = nullptr) {
+  const ssam_kernel_config c = b200_detail::to_c(cfg);
+  b200_detail::StencilArgs<T> sa(st);
+  b200_detail::check(ssam_b200_check_stencil2d(in.width, in.height, &sa.s, &c, iters));
+  Grid2D<T> out(in.width, in.height);
+  ssam_op_counters oc = b200_detail::to_c(counters);
+  b200_detail::check(ssam_b200_stencil2d_multi(
+      b200_detail::Dtype<T>::value, in.data.data(), in.width, in.height, &sa.s, &c, iters,
+      devices.data(), static_cast<int>(devices.size()), out.data.data(),
+      counters ? &oc : nullptr, nullptr));
+  b200_detail::from_c(oc, counters);
+  return out;
+}
+
+template <class T>
+Grid3D<T> stencil3d(const Grid3D<T>& in, const Stencil<T>& st, const KernelConfig& cfg,
+                    int iters, const std::vector<int>& devices, OpCounters* counters = nullptr) {
+  const ssam_kernel_config c = b200_detail::to_c(cfg);
+  b200_detail::StencilArgs<T> sa(st);
+  b200_detail::check(ssam_b200_check_stencil3d(in.nx, in.ny, in.nz, &sa.s, &c, iters));
+  Grid3D<T> out(in.nx, in.ny, in.nz);
+  ssam_op_counters oc = b200_detail::to_c(counters);
+  b200_detail::check(ssam_b200_stencil3d_multi(
+      b200_detail::Dtype<T>::value, in.data.data(), in.nx, in.ny, in.nz, &sa.s, &c, iters,
+      devices.data(), static_cast<int>(devices.size()), out.data.data(),
+      counters ? &oc : nullptr, nullptr));
   b200_detail::from_c(oc, counters);
   return out;
 }

@@ -177,6 +177,7 @@ class Reference:
         lib.ssam_ref_scan.argtypes = [_i, _p, _i, _i, _p, _p, _i]
         lib.ssam_ref_sgrd_write.argtypes = [_i, C.c_char_p, _i, _p, _p]
         lib.ssam_ref_sgrd_read.argtypes = [_i, C.c_char_p, _i, _p, _p, C.c_longlong]
+        lib.ssam_ref_profile.argtypes = [C.c_char_p, C.c_char_p, _i, _p, _i, _i, _p]
         self.lib = lib
 
     def max_threads(self) -> int:
@@ -279,6 +280,17 @@ class Reference:
             return rc, None
         shape = tuple(int(d) for d in dims[:rank][::-1])
         return 0, buf[:int(np.prod(shape))].reshape(shape).copy()
+
+
+    def profile(self, name_or_path: str, m: int = 3, n: int = 3):
+        """ssam::resolve_profile (perf_model.cpp:89-97) -> (status, name, six latencies,
+        (latency_reg, latency_smem) at m x n)."""
+        name = C.create_string_buffer(64)
+        vals = np.zeros(6, dtype=np.float64)
+        lat = np.zeros(2, dtype=np.float64)
+        rc = self.lib.ssam_ref_profile(name_or_path.encode(), name, 64, _ptr(vals), m, n,
+                                       _ptr(lat))
+        return rc, name.value.decode(), vals, lat
 
 
 def max_rel_err(got: np.ndarray, want: np.ndarray) -> float:

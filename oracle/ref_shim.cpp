@@ -18,6 +18,7 @@
 // 2 std::length_error, 9 anything else.
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -28,6 +29,7 @@
 #include "ssam/kernels.hpp"
 #include "ssam/oracle.hpp"
 #include "ssam/grid_io.hpp"
+#include "ssam/perf_model.hpp"
 
 #ifdef _OPENMP
 #include <omp.h>
@@ -341,6 +343,23 @@ int ssam_ref_sgrd_read(int dtype, const char* path, int rank, int* dims, void* o
     case I64: return sgrd_read_t<long long>(path, rank, dims, out, cap);
   }
   return 1;
+}
+
+// ssam::resolve_profile (perf_model.cpp:89-97: builtin name, then
+// $SSAM_PROFILE_DIR/<name>.profile, then a path) -> the six latencies as
+// doubles, the profile name, and the model's latency_reg / latency_smem
+// (perf_model.hpp:38-44) at m x n.
+int ssam_ref_profile(const char* name_or_path, char* name, int name_cap, double* vals, int m,
+                     int n, double* l_reg_smem) {
+  return guarded([&] {
+    const LatencyProfile p = resolve_profile(name_or_path);
+    std::snprintf(name, static_cast<size_t>(name_cap), "%s", p.name.c_str());
+    const Rational* r[6] = {&p.t_shfl, &p.t_mad, &p.t_smem_read, &p.t_reg, &p.t_gmem_read,
+                            &p.t_gmem_write};
+    for (int i = 0; i < 6; ++i) vals[i] = r[i]->to_double();
+    l_reg_smem[0] = latency_reg(m, n, p).to_double();
+    l_reg_smem[1] = latency_smem(m, n, p).to_double();
+  });
 }
 
 }  // extern "C"

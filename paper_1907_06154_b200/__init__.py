@@ -165,6 +165,8 @@ _sig("ssam_b200_ipc_alloc", [_sz, C.POINTER(_p), _p])
 _sig("ssam_b200_ipc_free", [_p])
 _sig("ssam_b200_ipc_open", [_p, C.POINTER(_p)])
 _sig("ssam_b200_ipc_close", [_p])
+_sig("ssam_b200_stream_write_u32", [_p, C.c_uint32, _p])
+_sig("ssam_b200_stream_wait_u32", [_p, C.c_uint32, _p])
 IPC_HANDLE_BYTES = 64
 
 lib = _lib  # raw handle for device-level callers (bench.py, tests)
@@ -173,7 +175,7 @@ lib = _lib  # raw handle for device-level callers (bench.py, tests)
 EXPORTED = [
     "ssam_b200_abi_version", "ssam_b200_last_error", "ssam_b200_device_count",
     "ssam_b200_default_config", "ssam_b200_launch_count", "ssam_b200_conv2d",
-    "ssam_b200_stencil2d_multi", "ssam_b200_stencil3d_multi",
+    "ssam_b200_stencil2d_multi", "ssam_b200_stencil3d_multi", "ssam_b200_measure_latency",
     "ssam_b200_stencil2d", "ssam_b200_stencil3d", "ssam_b200_check_conv2d",
     "ssam_b200_check_stencil2d", "ssam_b200_check_stencil3d", "ssam_b200_counters_conv2d",
     "ssam_b200_counters_stencil2d", "ssam_b200_counters_stencil3d", "ssam_b200_benchmark_count",
@@ -187,6 +189,7 @@ EXPORTED = [
     "ssam_b200_gather_conv2d", "ssam_b200_gather_stencil", "ssam_b200_stencil3d_tb",
     "ssam_b200_stencil3d_tb_max", "ssam_b200_stencil3d_sweep_peer", "ssam_b200_stencil3d_tb_peer",
     "ssam_b200_ipc_alloc", "ssam_b200_ipc_free", "ssam_b200_ipc_open", "ssam_b200_ipc_close",
+    "ssam_b200_stream_write_u32", "ssam_b200_stream_wait_u32",
     "ssam_b200_stencil2d_tb_range", "ssam_b200_gather_stencil_run", "ssam_b200_trim_cache",
     "ssam_b200_stencil_batch",
 ]
@@ -445,6 +448,36 @@ def stencil3d(grid: np.ndarray, st: Stencil, cfg: Optional[KernelConfig] = None,
     if counters is not None:
         counters._store(cnt)
     return out
+
+
+class _Latency(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("t_shfl", "t_mad", "t_smem_read", "t_reg",
+                                          "t_gmem_read", "t_gmem_write", "t_l2_read",
+                                          "sm_clock_mhz")]
+
+
+_sig("ssam_b200_measure_latency", [C.POINTER(_Latency)])
+
+PROFILE_FIELDS = ("t_shfl", "t_mad", "t_smem_read", "t_reg", "t_gmem_read", "t_gmem_write")
+
+
+def measure_latency_profile() -> dict:
+    """ssam::LatencyProfile fields (perf_model.hpp:14-26) measured on the
+    current device by csrc/latency.cu, in SM cycles (floats), plus t_l2_read
+    and sm_clock_mhz."""
+    r = _Latency()
+    _raise(_lib.ssam_b200_measure_latency(C.byref(r)))
+    return {n: getattr(r, n) for n, _ in _Latency._fields_}
+
+
+def format_profile(name: str, prof: dict) -> str:
+    """A profile file the reference's load_profile_file reads
+    (perf_model.cpp:41-78): `name`, then one `field value` line per latency,
+    values as integers (whole cycles) or `num/den` rationals."""
+    lines = [f"name {name}"]
+    for f in PROFILE_FIELDS:
+        lines.append(f"{f} {max(1, int(round(prof[f])))}")
+    return "\n".join(lines) + "\n"
 
 
 def stencil_multi(grid: np.ndarray, st: Stencil, devices: Sequence[int],

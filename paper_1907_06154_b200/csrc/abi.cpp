@@ -920,6 +920,24 @@ int ssam_b200_stencil3d(int dtype, const void* in, int nx, int ny, int nz, const
   return SSAM_OK;
 }
 
+int ssam_b200_measure_latency(ssam_latency_profile* out) {
+  g_err.clear();
+  if (!out) return fail(SSAM_ERR_INVALID_ARGUMENT, "measure_latency: null output");
+  if (int s = device_ready()) return s;
+  double t[8];
+  const cudaError_t e = measure_latency(t, cudaStreamPerThread);
+  if (e != cudaSuccess) return cuda_fail(e, "measure_latency");
+  out->t_shfl = t[0];
+  out->t_mad = t[1];
+  out->t_smem_read = t[2];
+  out->t_reg = t[3];
+  out->t_gmem_read = t[4];
+  out->t_gmem_write = t[5];
+  out->t_l2_read = t[6];
+  out->sm_clock_mhz = t[7];
+  return SSAM_OK;
+}
+
 int ssam_b200_stencil2d_multi(int dtype, const void* in, int w, int h, const ssam_stencil* st,
                               const ssam_kernel_config* cfg, int iters, const int* devices,
                               int ndev, void* out, ssam_op_counters* counters, int* used) {
@@ -1431,6 +1449,59 @@ int ssam_b200_ipc_close(void* d_ptr) {
   g_err.clear();
   const cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
   return e == cudaSuccess ? SSAM_OK : cuda_fail(e, "ipc_close");
+}
+
+// ---- stream memory operations (peer-halo generation flags) -------------------
+// cuStreamWriteValue32 / cuStreamWaitValue32 through the runtime's driver
+// entry points: the GPU front end performs the write after the stream's
+// prior work (with a memory barrier, so the kernel's peer stores are visible
+// first) and holds the stream until a 32-bit word reaches a value -- no SM
+// and no host round trip.
+}  // extern "C"
+namespace {
+using WriteValueFn = int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+using WaitValueFn = int (*)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+template <class F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<F>(p);
+}
+WriteValueFn write_value_fn() {
+  static WriteValueFn f = driver_fn<WriteValueFn>("cuStreamWriteValue32");
+  return f;
+}
+WaitValueFn wait_value_fn() {
+  static WaitValueFn f = driver_fn<WaitValueFn>("cuStreamWaitValue32");
+  return f;
+}
+constexpr unsigned kWaitGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ
+}  // namespace
+extern "C" {
+
+int ssam_b200_stream_write_u32(void* d_addr, uint32_t value, void* stream) {
+  g_err.clear();
+  if (!d_addr) return fail(SSAM_ERR_INVALID_ARGUMENT, "stream_write_u32: null address");
+  if (int s = device_ready()) return s;
+  WriteValueFn f = write_value_fn();
+  if (!f) return fail(SSAM_ERR_CUDA, "stream_write_u32: cuStreamWriteValue32 unavailable");
+  const int r = f(as_stream(stream), reinterpret_cast<unsigned long long>(d_addr), value, 0);
+  return r == 0 ? SSAM_OK : fail(SSAM_ERR_CUDA, "cuStreamWriteValue32 failed: " + std::to_string(r));
+}
+
+int ssam_b200_stream_wait_u32(const void* d_addr, uint32_t value, void* stream) {
+  g_err.clear();
+  if (!d_addr) return fail(SSAM_ERR_INVALID_ARGUMENT, "stream_wait_u32: null address");
+  if (int s = device_ready()) return s;
+  WaitValueFn f = wait_value_fn();
+  if (!f) return fail(SSAM_ERR_CUDA, "stream_wait_u32: cuStreamWaitValue32 unavailable");
+  const int r = f(as_stream(stream), reinterpret_cast<unsigned long long>(d_addr), value, kWaitGeq);
+  return r == 0 ? SSAM_OK : fail(SSAM_ERR_CUDA, "cuStreamWaitValue32 failed: " + std::to_string(r));
 }
 
 }  // extern "C"

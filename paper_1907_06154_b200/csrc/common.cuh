@@ -200,13 +200,23 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
-// TMA ring protocol used by every engine (the PTX memory-model pattern of a
-// producer/consumer mbarrier pipeline): a consumer lane reads a slot with
-// LDS, then arrives on the slot's EMPTY barrier (mbarrier.arrive has release
-// semantics); the issuing lane waits on it (try_wait has acquire
-// semantics), executes fence.proxy.async (generic-proxy reads ordered
-// before the async-proxy writes of the refill) and only then issues the
-// TMA copy into the slot.
+// TMA ring protocols (PTX memory model).  A slot read with LDS (generic
+// proxy) may only be refilled by TMA (async proxy) once every read is
+// ordered before the refill:
+//  * rings shared by several warps (engine3d.cuh, engine3d_pipe.cuh): each
+//    consumer lane arrives on the slot's EMPTY mbarrier (release); the
+//    producer waits on it (acquire), executes fence.proxy.async and issues
+//    the copy -- the producer/consumer mbarrier pipeline;
+//  * warp-private rings (engine2d.cuh, engine2d_fma.cuh, tb2d.cu):
+//    ring_release_warp() -- every lane executes fence.proxy.async after its
+//    reads, then the warp barrier orders all lanes before lane 0's copy (the
+//    fence-then-barrier-then-issue pattern of TMA stores, mirrored).  A/B on
+//    the 2D fused kernels: as fast as an unsynchronised hand-back, 4% faster
+//    than the mbarrier protocol (profiles/r02/ring_protocol_ab.txt).
+__device__ __forceinline__ void ring_release_warp() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+}
 
 // Q-vector shared load / global store as 16-byte chunks (Q*sizeof(T) in {16, 32}).
 template <class T, int Q>

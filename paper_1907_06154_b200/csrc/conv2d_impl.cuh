@@ -9,6 +9,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "engine2d_conv.cuh"
 #include "engine2d_fma.cuh"
 #include "launch.cuh"
 
@@ -106,7 +107,19 @@ bool fma_eligible(const Engine2DArgs<T>& a) {
 // RY = 4 up to 10x10 (+4..30%: shorter window shifts, 16 FMA chains),
 // RY = 2 at 11x11, RY = 1 beyond (the unrolled pass stays ~1600 FFMAs;
 // +3..10%).  The exact lane plan is used where it adds >= 1.5% columns.
-constexpr int fma_ry(int k) { return k <= 10 ? 4 : (k <= 11 ? 2 : 1); }
+#ifndef SSAM_CONV_RY_SMALL
+#define SSAM_CONV_RY_SMALL 4
+#endif
+#ifndef SSAM_CONV_FQ
+#define SSAM_CONV_FQ 4
+#endif
+#ifndef SSAM_CONV_CHAIN1_MIN
+#define SSAM_CONV_CHAIN1_MIN 7
+#endif
+#ifndef SSAM_CONV_RY11
+#define SSAM_CONV_RY11 2
+#endif
+constexpr int fma_ry(int k) { return k <= 10 ? SSAM_CONV_RY_SMALL : (k <= 11 ? SSAM_CONV_RY11 : 1); }
 constexpr bool fma_exact(int k, int q) {
   const int r = (k - 1) / 2, l = k - 1 - r, a = (l + q - 1) / q * q;
   const int v_aligned = (32 * q - r - a) / q * q, v_exact = 32 * q - (k - 1);
@@ -121,7 +134,7 @@ cudaError_t conv_fma_sq(const Engine2DArgs<T>& a, cudaStream_t s) {
   // (fp32 tolerance 1e-5).  Larger filters keep the two-level order, which
   // is what holds 17x17 and 20x20 under 1e-5; 6x6 measured
   // slower with it.
-  if constexpr (K >= 7 && K <= 11 && std::is_same<T, float>::value)
+  if constexpr (K >= SSAM_CONV_CHAIN1_MIN && K <= 11 && std::is_same<T, float>::value)
     return launch_fma2d<T, Q, K, K, fma_ry(K), fma_exact(K, Q), K * K, DenseMask, true>(a, s);
   return launch_fma2d<T, Q, K, K, fma_ry(K), fma_exact(K, Q), K * K>(a, s);
 }
@@ -130,11 +143,35 @@ template <class T, int Q, int N>
 cudaError_t conv_rt(const Engine2DArgs<T>& a, cudaStream_t s) {
   return launch_ssam2d<T, Q, N, 0, DenseMask, pf_rows(N), 20 * N>(a, s);
 }
+// K = 6..11 take the register-row engine (engine2d_conv.cuh) unless
+// SSAM_B200_CONV_REG=0.
+inline bool conv_reg_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SSAM_B200_CONV_REG");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+#ifndef SSAM_CONV_REG_MIN
+#define SSAM_CONV_REG_MIN 6
+#endif
+#ifndef SSAM_CONV_REG_MAX
+#define SSAM_CONV_REG_MAX 11
+#endif
+
 template <class T, int Q, int K>
 cudaError_t conv_sq(const Engine2DArgs<T>& a, cudaStream_t s) {
+  if constexpr (K >= SSAM_CONV_REG_MIN && K <= SSAM_CONV_REG_MAX) {
+    if (conv_reg_enabled() && a.bmode == kBndZero) {
+      const cudaError_t e = launch_conv2d_reg<T, K>(a.in, a.out, a.W, a.H, a.y_begin, a.y_end, a.coef, s);
+      if (e != cudaErrorNotSupported) return e;
+      cudaGetLastError();
+    }
+  }
   if constexpr (K >= 3) {
     const int kmin = conv_fma_min_k();
-    if (kmin > 0 && K >= kmin && fma_eligible(a)) return conv_fma_sq<T, Q == 8 ? 4 : Q, K>(a, s);
+    if (kmin > 0 && K >= kmin && fma_eligible(a))
+      return conv_fma_sq<T, (std::is_same<T, float>::value && K <= 11) ? SSAM_CONV_FQ : (Q == 8 ? 4 : Q), K>(a, s);
   }
   return launch_ssam2d<T, Q, K, K, DenseMask, pf_rows(K), K * K>(a, s);
 }

@@ -289,8 +289,8 @@ __device__ __forceinline__ void store_row(const Ssam2DParams<T, CAP>& p, const S
     if (sp.x0 + q >= sp.xlo && sp.x0 + q < sp.xhi) row[q] = acc[q];
 }
 
-// Shared memory of the TMA kernel: per warp D boxes of RB rows, D full
-// mbarriers and a 128-byte line holding the D empty mbarriers (D <= 16).
+// Shared memory of the TMA kernel: per warp D boxes of RB rows, D mbarriers
+// and a spare 128-byte line.
 template <class T, int Q, int RB, int D>
 __host__ __device__ constexpr size_t tma2d_smem(int warps) {
   return static_cast<size_t>(warps) *
@@ -319,16 +319,10 @@ __global__ void __launch_bounds__(128)
   uint64_t* bars = reinterpret_cast<uint64_t*>(
                        smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * BOX_BYTES) +
                    wib * D;
-  static_assert(D <= 16, "empty barriers fit the warp's 128-byte line");
-  uint64_t* empty = reinterpret_cast<uint64_t*>(
-      smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * (BOX_BYTES + 8) + wib * 128);
   if (lane == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
-    for (int s = 0; s < D; ++s) {
-      mbar_init(smem_u32(&bars[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 32);
-    }
+    for (int s = 0; s < D; ++s) mbar_init(smem_u32(&bars[s]), 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -344,18 +338,11 @@ __global__ void __launch_bounds__(128)
   };
   if (lane == 0)
     for (int j = 0; j < min(D, nbox); ++j) issue(j);
-  // Ring hand-back (PTX memory model): every lane arrives (release) on the
-  // slot's empty barrier after its last read of box j; lane 0 waits
-  // (acquire), fences generic -> async proxy, and refills the slot with
-  // box j + D.
+  // Ring hand-back after the warp's last read of box j (common.cuh
+  // ring_release_warp): the slot is refilled with box j + D.
   auto recycle = [&](int j) {
-    const int s = j % D;
-    mbar_arrive(smem_u32(&empty[s]));
-    if (lane == 0 && j + D < nbox) {
-      mbar_wait(smem_u32(&empty[s]), (j / D) & 1);
-      fence_proxy_async();
-      issue(j + D);
-    }
+    ring_release_warp();
+    if (lane == 0 && j + D < nbox) issue(j + D);
   };
 
   if constexpr (RB == NR) {

@@ -38,8 +38,8 @@
 // Rows arrive as RB-row TMA boxes (zero fill = zero boundary) in a per-warp
 // ring of D slots.  A box is handed back once its rows have fed a pass's
 // FFMAs (so its LDS have returned); in the prologue, where the window is
-// taller than the ring, as soon as its rows were read (every lane arrives
-// on the slot's empty barrier; lane 0 acquires it before the refill).
+// taller than the ring, as soon as its rows were read (common.cuh
+// ring_release_warp before lane 0 refills the slot).
 #pragma once
 
 #include "engine2d.cuh"
@@ -123,9 +123,6 @@ __global__ void __launch_bounds__(128)
   uint64_t* bars =
       reinterpret_cast<uint64_t*>(smem_raw + static_cast<size_t>(nwarps) * D * SLOT_BYTES) +
       wib * D;
-  static_assert(D <= 16, "empty barriers fit the warp's 128-byte line");
-  uint64_t* empty = reinterpret_cast<uint64_t*>(
-      smem_raw + static_cast<size_t>(nwarps) * D * (SLOT_BYTES + 8) + wib * 128);
   T* scoef = reinterpret_cast<T*>(smem_raw +
                                   static_cast<size_t>(nwarps) * (D * (SLOT_BYTES + 8) + 128));
   if constexpr (!UNROLL) {
@@ -159,10 +156,7 @@ __global__ void __launch_bounds__(128)
   if (lane == 0) {
     prefetch_tmap(&P.tmap);
 #pragma unroll
-    for (int s = 0; s < D; ++s) {
-      mbar_init(smem_u32(&bars[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 32);
-    }
+    for (int s = 0; s < D; ++s) mbar_init(smem_u32(&bars[s]), 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -179,16 +173,11 @@ __global__ void __launch_bounds__(128)
   };
   if (lane == 0)
     for (int b = 0; b < min(D, nbox); ++b) issue(b);
-  // Ring hand-back (PTX memory model): every lane arrives (release) on box
-  // b's empty barrier after its last read of it; lane 0 waits (acquire),
-  // fences generic -> async proxy and refills the slot with box b + D.
+  // Ring hand-back after the warp's last read of box b (common.cuh
+  // ring_release_warp): the slot is refilled with box b + D.
   auto recycle = [&](int b) {
-    mbar_arrive(smem_u32(&empty[b % D]));
-    if (lane == 0 && b + D < nbox) {
-      mbar_wait(smem_u32(&empty[b % D]), (b / D) & 1);
-      fence_proxy_async();
-      issue(b + D);
-    }
+    ring_release_warp();
+    if (lane == 0 && b + D < nbox) issue(b + D);
   };
   auto row_ptr = [&](int s) -> const T* {
     const int b = s / RB;

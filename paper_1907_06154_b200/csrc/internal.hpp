@@ -127,6 +127,10 @@ cudaError_t conv1d_device(const T* d_in, T* d_out, int len, const T* h_w, int m,
 template <class T>
 cudaError_t scan_device(const T* d_in, T* d_out, size_t n, cudaStream_t s);
 
+// ---- latency micro-benchmarks (latency.cu): t[0..7] = t_shfl, t_mad,
+// t_smem_read, t_reg, t_gmem_read, t_gmem_write, t_l2_read (cycles), SM MHz
+cudaError_t measure_latency(double* t, cudaStream_t s);
+
 // ---- utilities --------------------------------------------------------------
 cudaError_t fill_random(int dtype, void* d, std::size_t count, std::uint64_t seed,
                         std::uint64_t first, cudaStream_t s);

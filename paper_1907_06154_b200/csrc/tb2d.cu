@@ -79,16 +79,10 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
   uint64_t* bars = reinterpret_cast<uint64_t*>(
                        smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * BOX_BYTES) +
                    wib * D;
-  static_assert(D <= 16, "empty barriers fit the warp's 128-byte line");
-  uint64_t* empty = reinterpret_cast<uint64_t*>(
-      smem_raw + static_cast<size_t>(blockDim.x >> 5) * D * (BOX_BYTES + 8) + wib * 128);
   if (lane == 0) {
     prefetch_tmap(&p.tmap);
 #pragma unroll
-    for (int s = 0; s < D; ++s) {
-      mbar_init(smem_u32(&bars[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 32);
-    }
+    for (int s = 0; s < D; ++s) mbar_init(smem_u32(&bars[s]), 1);
     fence_mbar_init();
   }
   __syncwarp();
@@ -157,14 +151,11 @@ __global__ void __launch_bounds__(128) tb2d_kernel(const __grid_constant__ Tb2DP
         }
       }
     }
-    // ring hand-back: every lane releases the slot after its reads, lane 0
-    // acquires, fences generic -> async proxy and refills it
-    mbar_arrive(smem_u32(&empty[s]));
-    if (lane == 0 && j + D < nbox) {
-      mbar_wait(smem_u32(&empty[s]), (j / D) & 1);
-      fence_proxy_async();
-      issue(j + D);
-    }
+    // ring hand-back (PTX memory model): every lane orders its reads of the
+    // slot before later async-proxy writes (fence.proxy.async), the warp
+    // barrier orders all lanes before lane 0, which then refills the slot
+    ring_release_warp();
+    if (lane == 0 && j + D < nbox) issue(j + D);
   }
 }
 
@@ -209,7 +200,7 @@ cudaError_t launch_tb(const T* in, T* out, int W, int H, int yb, int ye, int rlo
   std::memcpy(p.coef, c.data(), sizeof(T) * CAP);
   cudaError_t e = make_tmap_2d(&p.tmap, in, sizeof(T), W, H, sizeof(T) * W, 32 * Q, RB);
   if (e != cudaSuccess) return e;
-  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * (D * (RB * 32 * Q * sizeof(T) + 8) + 128);
+  const size_t smem = static_cast<size_t>(kWarpsPerBlock) * D * (RB * 32 * Q * sizeof(T) + 8);
   const dim3 grid((p.nstrips + kWarpsPerBlock - 1) / kWarpsPerBlock, (rows + p.seg - 1) / p.seg);
   e = launch_pdl(tb2d_kernel<T, Q, K, Mask, TB, RB, D, CAP>, grid, dim3(32 * kWarpsPerBlock), smem,
                  s, p);

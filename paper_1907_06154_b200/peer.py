@@ -13,11 +13,14 @@ transfer rides on the kernel's own stores, tile by tile.
 Ordering.  Sweep t of rank r writes neighbour buffers that the neighbour read
 in its sweep t-1 (ping-pong parity), and reads ghosts the neighbours wrote in
 their sweep t-1.  So every sweep waits, on the device, for the neighbours'
-previous sweep: each rank records an interprocess CUDA event after a sweep,
-a host barrier (gloo) makes every record visible before anyone issues the
-matching waits, and two events alternate so a rank running one sweep ahead
-never re-records an event a neighbour has yet to wait on.  The host barrier
-does not wait for the GPU; the device queue stays full.
+previous sweep, through generation flags: each rank owns two 32-bit words
+(IPC memory, one per neighbour); after its sweep t a rank's stream writes
+t+1 into the word each neighbour keeps for it (cuStreamWriteValue32, after
+the sweep's peer stores are visible), and before sweep t+1 its stream waits
+until both of its own words are >= t+1 (cuStreamWaitValue32).  No host
+barrier per sweep: the host only enqueues, the GPU front end does the
+waiting.  (SSAM_PEER_HOST_BARRIER=1 selects the previous protocol:
+interprocess events made visible by a gloo barrier per sweep.)
 
 Layout and decomposition are slab.py's (Slab, decompose, fill_slab): local
 plane p is global plane z_first - ghost + p, ghost = k * Tb.
@@ -25,6 +28,7 @@ plane p is global plane z_first - ghost + p, ghost = k * Tb.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional
 
 import numpy as np
@@ -91,19 +95,31 @@ class PeerSlabRunner:
         self.shape = (slab.nz_local, ny, nx)
         self.bufs = [IpcBuffer(self.shape, dtype), IpcBuffer(self.shape, dtype)]
         self.events = [torch.cuda.Event(interprocess=True) for _ in range(2)]
+        # generation flags: word 0 written by rank-1, word 1 by rank+1
+        self.flags = IpcBuffer((2,), torch.int64)
+        self.flags.tensor.zero_()
+        torch.cuda.synchronize()  # zeroed before any neighbour can signal
+        self.host_barrier = os.environ.get("SSAM_PEER_HOST_BARRIER", "0") == "1"
+        self.gen = 0
         dev_idx = torch.cuda.current_device()
         info = {"nz_own": slab.nz_own, "bufs": [b.handle for b in self.bufs],
+                "flags": self.flags.handle,
                 "events": [bytes(e.ipc_handle()) for e in self.events]}
         allinfo = [None] * slab.world
         dist.all_gather_object(allinfo, info, group=group)
         below = allinfo[slab.rank - 1]["nz_own"] if slab.rank > 0 else 0
         lo_shift, lo_end, hi_shift, hi_begin = peer_geometry(slab, below, nx * ny)
         self.opened = []
+        self.nb_flags = []  # (address of my word in the neighbour's flags)
         self.nb_events = [[], []]
         self.halo = [_PeerHalo(), _PeerHalo()]
         for side, nb in ((0, slab.rank - 1), (1, slab.rank + 1)):
             if not 0 <= nb < slab.world:
                 continue
+            fptr = _open(allinfo[nb]["flags"])
+            self.opened.append(fptr)
+            # rank-1 keeps my word at index 1 (from its upper neighbour), rank+1 at 0
+            self.nb_flags.append(fptr + (8 if side == 0 else 0))
             for j in range(2):
                 ptr = _open(allinfo[nb]["bufs"][j])
                 self.opened.append(ptr)
@@ -125,8 +141,20 @@ class PeerSlabRunner:
         return self.bufs[1].tensor
 
     def _publish(self, stream) -> None:
-        """Record this rank's event for the work queued so far and wait (on the
-        device) for the neighbours' matching records."""
+        """Signal the neighbours that the work queued so far is done and make
+        the stream wait (on the device) until they signalled the same
+        generation."""
+        if not self.host_barrier:
+            self.gen += 1
+            sp = C.c_void_p(stream.cuda_stream)
+            for addr in self.nb_flags:
+                _raise(lib.ssam_b200_stream_write_u32(C.c_void_p(addr), self.gen, sp))
+            s = self.slab
+            for word, nb in ((0, s.rank - 1), (1, s.rank + 1)):
+                if 0 <= nb < s.world:
+                    _raise(lib.ssam_b200_stream_wait_u32(
+                        C.c_void_p(self.flags.ptr + 8 * word), self.gen, sp))
+            return
         p = self._parity
         self.events[p].record(stream)
         dist.barrier(group=self.group)
@@ -178,4 +206,5 @@ class PeerSlabRunner:
         dist.barrier(group=self.group)  # every mapping of our buffers is closed
         for b in self.bufs:
             b.free()
+        self.flags.free()
         self.bufs = []

@@ -251,6 +251,35 @@ int main() {
         [&] { stencil3d(random_grid3d<double>(32, 12, 3, 1), make_benchmark_stencil("3d13pt"), ok, 1); }));
   });
 
+  // ---- device-set overloads (multi.cpp): slabs sharing device 0 here ----------
+  run("stencil3d on a device set equals the one-device call bit for bit", [] {
+    for (const char* name : {"3d7pt", "3d13pt", "3d27pt", "poisson"}) {
+      auto st = convert_stencil<float>(make_benchmark_stencil(name));
+      auto g = random_grid3d<float>(64, 24, 50, 77);
+      KernelConfig cfg;
+      cfg.p = 2;
+      cfg.b = 32 * (2 * st.order + 2);
+      OpCounters c1, c2;
+      auto one = stencil3d(g, st, cfg, 5, &c1);
+      auto many = stencil3d(g, st, cfg, 5, std::vector<int>{0, 0, 0}, &c2);
+      CHECK(one.data == many.data);
+      CHECK(c1.mads == c2.mads && c1.shuffles == c2.shuffles);
+    }
+    CHECK(throws<std::invalid_argument>([&] {
+      stencil3d(random_grid3d<double>(32, 32, 32, 1), make_benchmark_stencil("3d7pt"),
+                KernelConfig{}, 1, std::vector<int>{});
+    }));
+  });
+  run("stencil2d on a device set equals the one-device call bit for bit", [] {
+    for (const char* name : {"2d5pt", "2d9pt", "2ds25pt"}) {
+      auto st = make_benchmark_stencil(name);
+      auto g = random_grid2d<double>(200, 160, 5);
+      KernelConfig cfg;
+      CHECK(stencil2d(g, st, cfg, 7).data ==
+            stencil2d(g, st, cfg, 7, std::vector<int>{0, 0}).data);
+    }
+  });
+
   // ---- proj/tests/acceptance.cpp criteria 1 and 2 ------------------------------
   run("acceptance: oracle-equivalence-convolution", [] {
     std::vector<std::pair<int, int>> shapes;

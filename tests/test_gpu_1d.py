@@ -113,3 +113,14 @@ def test_scan_large_multi_tile(cuda_lib, orc):
         scale = np.maximum(1.0, np.maximum.accumulate(np.abs(exact))).astype(np.float64)
         got = cuda_lib.scan(x).astype(np.longdouble)
         assert float(np.max(np.abs(got - exact) / scale)) <= tol, dt
+
+
+def test_scan_deterministic(cuda_lib, orc):
+    """One-pass scan with the canonical carry tree (scan.cu): repeated runs are
+    bit-identical for floating point too, whatever the tile timing."""
+    n = (1 << 22) + 96
+    for dt in (np.float32, np.float64):
+        x = orc.random_grid(n, dt, 12)
+        first = cuda_lib.scan(x)
+        for _ in range(4):
+            assert np.array_equal(cuda_lib.scan(x), first)
