@@ -143,7 +143,8 @@ template <class T, int Q, int N>
 cudaError_t conv_rt(const Engine2DArgs<T>& a, cudaStream_t s) {
   return launch_ssam2d<T, Q, N, 0, DenseMask, pf_rows(N), 20 * N>(a, s);
 }
-// K = 6..11 take the register-row engine (engine2d_conv.cuh) unless
+// K = 6..15 take the register-row engine (engine2d_conv.cuh; 16+ lose to
+// the two-level chain engine, profiles/r02/conv_reg_big_ab.txt) unless
 // SSAM_B200_CONV_REG=0.
 inline bool conv_reg_enabled() {
   static const bool v = [] {
@@ -156,7 +157,7 @@ inline bool conv_reg_enabled() {
 #define SSAM_CONV_REG_MIN 6
 #endif
 #ifndef SSAM_CONV_REG_MAX
-#define SSAM_CONV_REG_MAX 11
+#define SSAM_CONV_REG_MAX 15
 #endif
 
 template <class T, int Q, int K>

@@ -30,6 +30,10 @@
 
 #include "launch.cuh"
 
+#ifndef SSAM_CONVREG_TWO_MIN
+#define SSAM_CONVREG_TWO_MIN 12
+#endif
+
 namespace ssam_b200 {
 
 template <class T, int K, int Q>
@@ -38,14 +42,21 @@ struct ConvRegGeom {
   static constexpr int R = (K - 1) / 2, L = K - 1 - R;         // columns right / left of an output
   static constexpr int HL = (L + V - 1) / V * V;               // box pad left (whole chunks)
   static constexpr int HR = (R + V - 1) / V * V;               // box pad right
-  static constexpr int BW = HL + 32 * Q + HR;                  // box / smem row width
+  // a TMA box is at most 256 elements wide: a warp strip of 32 Q columns
+  // is staged as NSUB overlapping sub-boxes, each serving SUBL lanes
+  static constexpr int NSUB = (HL + 32 * Q + HR) <= 256 ? 1 : 2;
+  static constexpr int SUBL = 32 / NSUB;
+  static constexpr int BW = HL + SUBL * Q + HR;                // sub-box / smem row width
   static constexpr int OFF = HL - L;                           // lane's first column in its chunks
   static constexpr int NC = (OFF + Q + K - 1 + V - 1) / V;     // chunks a lane reads per row
-  // one ring slot: RB rows, padded to TMA's 128-byte destination alignment
+  // one sub-box of RB rows, padded to TMA's 128-byte destination alignment;
+  // a ring slot holds NSUB of them
   template <int RB>
-  static constexpr int slot_elems() {
+  static constexpr int sub_elems() {
     return static_cast<int>((RB * BW * sizeof(T) + 127) / 128 * 128 / sizeof(T));
   }
+  template <int RB>
+  static constexpr int slot_elems() { return NSUB * sub_elems<RB>(); }
   static_assert(BW <= 256, "TMA box width");
   static_assert(Q % V == 0, "whole chunks per lane");
 };
@@ -69,6 +80,10 @@ __global__ void __launch_bounds__(128)
   constexpr uint32_t BOX_BYTES = RB * BW * sizeof(T);
   constexpr int SLOT = G::template slot_elems<RB>();
   static_assert(RB == RY, "pass p starts at the first row of box p");
+  // large filters sum each input row's K taps first, then add the row
+  // partials -- the paper's two-level order transposed,
+  // which is what keeps fp32 within 1e-5 at 17x17 .. 20x20
+  constexpr bool TWO = K >= SSAM_CONVREG_TWO_MIN;
   constexpr int NB = (NIN - 1) / RB + 1;  // boxes a pass reads
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -101,13 +116,18 @@ __global__ void __launch_bounds__(128)
   auto issue = [&](int b) {
     const int s = b % D;
     const uint32_t bar = smem_u32(&bars[s]);
-    mbar_arrive_expect_tx(bar, BOX_BYTES);
-    tma_load_2d(smem_u32(ring + s * SLOT), &p.tmap, xb, y0 - U + b * RB, bar);
+    mbar_arrive_expect_tx(bar, BOX_BYTES * G::NSUB);
+#pragma unroll
+    for (int k = 0; k < G::NSUB; ++k)
+      tma_load_2d(smem_u32(ring + s * SLOT + k * G::template sub_elems<RB>()), &p.tmap,
+                  xb + k * G::SUBL * Q, y0 - U + b * RB, bar);
   };
   if (lane == 0)
     for (int b = 0; b < min(D, nbox); ++b) issue(b);
   int ready = 0;  // boxes waited for
-  const T* lane_base = ring + Q * lane;  // a lane's chunks start at box column Q*lane
+  // a lane's chunks start at column Q * (lane % SUBL) of its sub-box
+  const T* lane_base =
+      ring + (lane / G::SUBL) * G::template sub_elems<RB>() + Q * (lane % G::SUBL);
   int cslot = 0;                         // ring slot of box `pass`
 
   for (int pass = 0; pass < npass; ++pass) {
@@ -145,11 +165,26 @@ __global__ void __launch_bounds__(128)
       for (int r = 0; r < RY; ++r) {
         const int t = i - r;  // filter row of input row i for output row r
         if (t < 0 || t >= K) continue;
+        if constexpr (TWO) {
+          // two-level: the row's K-tap partial, then one add into the output
+          T rp[Q];
 #pragma unroll
-        for (int j = 0; j < K; ++j) {
-          const T c = p.coef[j * K + t];
+          for (int q = 0; q < Q; ++q) rp[q] = p.coef[t] * x[OFF + q];
 #pragma unroll
-          for (int q = 0; q < Q; ++q) acc[r][q] = fma_t(c, x[OFF + q + j], acc[r][q]);
+          for (int j = 1; j < K; ++j) {
+            const T c = p.coef[j * K + t];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) rp[q] = fma_t(c, x[OFF + q + j], rp[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < Q; ++q) acc[r][q] += rp[q];
+        } else {
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const T c = p.coef[j * K + t];
+#pragma unroll
+            for (int q = 0; q < Q; ++q) acc[r][q] = fma_t(c, x[OFF + q + j], acc[r][q]);
+          }
         }
       }
     }
@@ -175,9 +210,18 @@ __global__ void __launch_bounds__(128)
 
 template <class T, int K>
 struct ConvRegCfg {
-  static constexpr int Q = 16 / sizeof(T) * (sizeof(T) == 4 ? 1 : 1);  // fp32 4, fp64 2
-  static constexpr int RY = 4;
-  static constexpr int RB = 4;
+#ifndef SSAM_CONVREG_Q32
+#define SSAM_CONVREG_Q32 4
+#endif
+  static constexpr int Q = sizeof(T) == 4 ? SSAM_CONVREG_Q32 : 2;
+#ifndef SSAM_CONVREG_RY
+#define SSAM_CONVREG_RY 4
+#endif
+#ifndef SSAM_CONVREG_RY_BIG
+#define SSAM_CONVREG_RY_BIG 2
+#endif
+  static constexpr int RY = K <= 11 ? SSAM_CONVREG_RY : SSAM_CONVREG_RY_BIG;
+  static constexpr int RB = RY;
   // rows kept for the window (K - 1) + one pass in flight + prefetch
   static constexpr int D = (K - 1 + RB - 1) / RB + 3;
 };

@@ -100,7 +100,11 @@ struct PipeGeom {
 #endif
   // input / intermediate ring depth: a stage holds the 2K+1 planes of its
   // first step before it releases any, so a ring needs at least 2K+1 slots
-  static constexpr int DZ = SSAM_STAR_DZ > 2 * K + 2 ? SSAM_STAR_DZ : 2 * K + 2;
+#ifndef SSAM_STAR_DZ1
+#define SSAM_STAR_DZ1 SSAM_STAR_DZ
+#endif
+  static constexpr int DZW = TB == 1 ? SSAM_STAR_DZ1 : SSAM_STAR_DZ;
+  static constexpr int DZ = DZW > 2 * K + 2 ? DZW : 2 * K + 2;
   static constexpr int DI = SSAM_STAR_DI > 2 * K + 1 ? SSAM_STAR_DI : 2 * K + 1;
   static constexpr int cmax(int a, int b) { return a > b ? a : b; }
   static constexpr int IN_ROWS = cmax(sy(1) * ry(1) + 2 * K, nr(1) + 2 * K);
