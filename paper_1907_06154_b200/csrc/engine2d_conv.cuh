@@ -28,6 +28,8 @@
 // only from 17x17).
 #pragma once
 
+#include <type_traits>
+
 #include "launch.cuh"
 
 #ifndef SSAM_CONVREG_TWO_MIN
@@ -67,10 +69,30 @@ struct alignas(64) ConvRegParams {
   T* out;
   int W, H;
   int nstrips, seg, y_begin, y_end;
-  T coef[CAP];  // coef[j*K + t]
+  int xlo, xhi;  // written columns (stencils: the interior [k, W-k))
+  T coef[CAP];   // coef[j*K + t]
 };
 
-template <class T, int K, int Q, int RY, int RB, int D, int CAP>
+// Does input row i of a pass (RY output rows, K-row footprint) need chunk c
+// of the lane's columns?  (A chunk is read only if some tap of the mask
+// lands in it -- a star's off-centre rows need just the lane's own columns.)
+template <class Mask, int K, int Q, int RY, int OFF, int V>
+__host__ __device__ constexpr bool row_needs_chunk(int i, int c) {
+  for (int r = 0; r < RY; ++r) {
+    const int t = i - r;
+    if (t < 0 || t >= K) continue;
+    for (int j = 0; j < K; ++j) {
+      if (!Mask::has(j, t)) continue;
+      for (int q = 0; q < Q; ++q) {
+        const int col = OFF + q + j;
+        if (col >= c * V && col < c * V + V) return true;
+      }
+    }
+  }
+  return false;
+}
+
+template <class T, int K, int Q, int RY, int RB, int D, int CAP, class Mask = DenseMask>
 __global__ void __launch_bounds__(128)
     conv2d_reg_kernel(const __grid_constant__ ConvRegParams<T, CAP> p) {
   using G = ConvRegGeom<T, K, Q>;
@@ -83,7 +105,7 @@ __global__ void __launch_bounds__(128)
   // large filters sum each input row's K taps first, then add the row
   // partials -- the paper's two-level order transposed,
   // which is what keeps fp32 within 1e-5 at 17x17 .. 20x20
-  constexpr bool TWO = K >= SSAM_CONVREG_TWO_MIN;
+  constexpr bool TWO = K >= SSAM_CONVREG_TWO_MIN && std::is_same<Mask, DenseMask>::value;
   constexpr int NB = (NIN - 1) / RB + 1;  // boxes a pass reads
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -158,6 +180,7 @@ __global__ void __launch_bounds__(128)
       T x[NC * V];
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
+        if (!row_needs_chunk<Mask, K, Q, RY, OFF, V>(i, c)) continue;
         const int4 w = *reinterpret_cast<const int4*>(rowp + c * V);
         memcpy(&x[c * V], &w, 16);
       }
@@ -167,6 +190,7 @@ __global__ void __launch_bounds__(128)
         if (t < 0 || t >= K) continue;
         if constexpr (TWO) {
           // two-level: the row's K-tap partial, then one add into the output
+          static_assert(std::is_same<Mask, DenseMask>::value, "two-level order: dense filters");
           T rp[Q];
 #pragma unroll
           for (int q = 0; q < Q; ++q) rp[q] = p.coef[t] * x[OFF + q];
@@ -181,6 +205,7 @@ __global__ void __launch_bounds__(128)
         } else {
 #pragma unroll
           for (int j = 0; j < K; ++j) {
+            if (!Mask::has(j, t)) continue;
             const T c = p.coef[j * K + t];
 #pragma unroll
             for (int q = 0; q < Q; ++q) acc[r][q] = fma_t(c, x[OFF + q + j], acc[r][q]);
@@ -193,12 +218,12 @@ __global__ void __launch_bounds__(128)
     for (int r = 0; r < RY; ++r) {
       if (y + r >= y1) break;
       T* o = p.out + static_cast<size_t>(y + r) * p.W + x0;
-      if (x0 + Q <= p.W) {
+      if (x0 >= p.xlo && x0 + Q <= p.xhi) {
         st_q<T, Q>(o, acc[r]);
       } else {
 #pragma unroll
         for (int q = 0; q < Q; ++q)
-          if (x0 + q < p.W) o[q] = acc[r][q];
+          if (x0 + q >= p.xlo && x0 + q < p.xhi) o[q] = acc[r][q];
       }
     }
     // box `pass` lies wholly above the next pass's first row: hand it back
@@ -208,7 +233,15 @@ __global__ void __launch_bounds__(128)
   }
 }
 
-template <class T, int K>
+template <class Mask, int K>
+constexpr int mask_tap_count() {
+  int n = 0;
+  for (int j = 0; j < K; ++j)
+    for (int t = 0; t < K; ++t) n += Mask::has(j, t) ? 1 : 0;
+  return n;
+}
+
+template <class T, int K, class Mask = DenseMask>
 struct ConvRegCfg {
 #ifndef SSAM_CONVREG_Q32
 #define SSAM_CONVREG_Q32 4
@@ -220,16 +253,19 @@ struct ConvRegCfg {
 #ifndef SSAM_CONVREG_RY_BIG
 #define SSAM_CONVREG_RY_BIG 2
 #endif
-  static constexpr int RY = K <= 11 ? SSAM_CONVREG_RY : SSAM_CONVREG_RY_BIG;
+  static constexpr int RY = mask_tap_count<Mask, K>() <= 121 ? SSAM_CONVREG_RY : SSAM_CONVREG_RY_BIG;
   static constexpr int RB = RY;
   // rows kept for the window (K - 1) + one pass in flight + prefetch
   static constexpr int D = (K - 1 + RB - 1) / RB + 3;
 };
 
-template <class T, int K>
+// conv2d (Mask = DenseMask, every column written) and 2D stencils (a tap
+// mask, only the interior [ring, W - ring) written; rows are clamped by the
+// caller).
+template <class T, int K, class Mask = DenseMask>
 cudaError_t launch_conv2d_reg(const T* in, T* out, int W, int H, int y_begin, int y_end,
-                              const T* coef, cudaStream_t s) {
-  using C = ConvRegCfg<T, K>;
+                              const T* coef, cudaStream_t s, int ring = 0) {
+  using C = ConvRegCfg<T, K, Mask>;
   using G = ConvRegGeom<T, K, C::Q>;
   constexpr int CAP = K * K;
   if (W % G::V != 0 || !aligned16(in) || !aligned16(out)) return cudaErrorNotSupported;
@@ -244,10 +280,12 @@ cudaError_t launch_conv2d_reg(const T* in, T* out, int W, int H, int y_begin, in
   p.seg = (pick_seg(rows, p.nstrips, K) + C::RY - 1) / C::RY * C::RY;
   p.y_begin = y_begin;
   p.y_end = y_end;
+  p.xlo = ring;
+  p.xhi = W - ring;
   std::memcpy(p.coef, coef, sizeof(T) * CAP);
   cudaError_t e = make_tmap_2d(&p.tmap, in, sizeof(T), W, H, sizeof(T) * W, G::BW, C::RB);
   if (e != cudaSuccess) return e;
-  auto kern = conv2d_reg_kernel<T, K, C::Q, C::RY, C::RB, C::D, CAP>;
+  auto kern = conv2d_reg_kernel<T, K, C::Q, C::RY, C::RB, C::D, CAP, Mask>;
   const size_t smem =
       static_cast<size_t>(kWarpsPerBlock) * C::D * (G::template slot_elems<C::RB>() * sizeof(T) + 8);
   if (smem > 48 * 1024) {

@@ -74,6 +74,35 @@ struct PoissonMask3 {
   }
 };
 
+// coef[(l*M + j)*M + t] with l = dz+K, j = dx+K, t = dy+K (engine3d.cuh)
+template <int K>
+__host__ __device__ constexpr int cidx(int dx, int dy, int dz) {
+  return ((dz + K) * (2 * K + 1) + (dx + K)) * (2 * K + 1) + (dy + K);
+}
+
+// ---- the star's per-cell chain (shared by every 3D star kernel: the
+// pipeline engine, its direct-load kernel and the halo-lane kernel, so all
+// of them give bit-identical results for the same number of sweeps) --------
+
+// Star of order K: centre, then the x taps (dx = -K..-1, 1..K), the y taps,
+// the z taps -- first product rounded, then one FMA per tap.  xv/yv/zv(d)
+// return the sample at offset d on that axis.
+template <class T, int K, class P, class FX, class FY, class FZ>
+__device__ __forceinline__ T pipe_star_cell(const P& p, T c, FX xv, FY yv, FZ zv) {
+  T v = mul_t(p.coef[cidx<K>(0, 0, 0)], c);
+#pragma unroll
+  for (int d = -K; d <= K; ++d)
+    if (d != 0) v = fma_t(p.coef[cidx<K>(d, 0, 0)], xv(d), v);
+#pragma unroll
+  for (int d = -K; d <= K; ++d)
+    if (d != 0) v = fma_t(p.coef[cidx<K>(0, d, 0)], yv(d), v);
+#pragma unroll
+  for (int d = -K; d <= K; ++d)
+    if (d != 0) v = fma_t(p.coef[cidx<K>(0, 0, d)], zv(d), v);
+  return v;
+}
+
+
 // Stores one lane's Q outputs of row (z, y) at column x0 (vector when `vec`,
 // else only the columns inside [xlo, xhi)), and mirrors planes a neighbour
 // keeps as ghost slots into its buffer over peer memory.
@@ -623,6 +652,32 @@ __global__ void __launch_bounds__((halo3d_max_threads<T, K, Mask>()),
       if (z >= z1) break;
       take(z - z0 + 2 * K, pl[(ph + NPL - 1) % NPL], hp[(ph + NPL - 1) % NPL]);
       const bool mirror = PEER && mirrored3(p, z);
+      if constexpr (std::is_same<Mask, StarMask3<1>>::value) {
+        // the 7-point star: the pipeline engine's per-cell chain
+        // (pipe_star_cell), so single sweeps here equal the fused pipeline
+        // kernels bit for bit; x neighbours from the neighbour lanes, and
+        // at the warp's ends from the halo lanes' columns
+#pragma unroll
+        for (int r = 0; r < RY; ++r) {
+          const T(&cr)[Q] = pl[(ph + K) % NPL][r + K];
+          const T hc = hp[(ph + K) % NPL][r + K][0];
+          const T up = shfl_up(cr[Q - 1], 1);
+          const T dn = __shfl_down_sync(kFull, cr[0], 1);
+          const T lft = lane == 0 ? hc : up;
+          const T rgt = is_r ? hc : dn;
+          T acc1[Q];
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            auto xv = [&](int d) { return q + d < 0 ? lft : (q + d >= Q ? rgt : cr[q + d]); };
+            auto yv = [&](int d) { return pl[(ph + K) % NPL][r + K + d][q]; };
+            auto zv = [&](int d) { return pl[(ph + K + d) % NPL][r + K][q]; };
+            acc1[q] = pipe_star_cell<T, 1>(p, cr[q], xv, yv, zv);
+          }
+          const int y = y_out0 + r;
+          if (y < yhi) store_row3<T, Q>(p, z, y, x0, acc1, vec, xlo, xhi, mirror);
+        }
+        continue;
+      }
 #pragma unroll
       for (int r0 = 0; r0 < RY; r0 += HRG) {
         // halo chains: inj[g][m] = h_m(K-1), h_m(c) = h_{m-1}(c-1) + colpart_m(c)

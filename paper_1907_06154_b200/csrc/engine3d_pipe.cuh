@@ -54,12 +54,6 @@ struct PipeBox {
   using Mask = Mask_;
 };
 
-// coef[(l*M + j)*M + t] with l = dz+K, j = dx+K, t = dy+K (engine3d.cuh)
-template <int K>
-__host__ __device__ constexpr int cidx(int dx, int dy, int dz) {
-  return ((dz + K) * (2 * K + 1) + (dx + K)) * (2 * K + 1) + (dy + K);
-}
-
 // Geometry of one (T, shape, TB) pipeline.  Stage s (1..TB) has sy(s)
 // warps of ry(s) rows; sy(s) * ry(s) >= nr(s) = ROWS + 2 K (TB - s).
 template <class T, class Sh, int TB_>
@@ -159,24 +153,6 @@ template <class G> __device__ __forceinline__ int bi_empty(int s) {
 }
 
 // ---- the per-cell chains (shared by the pipeline and the direct kernel) ----
-
-// Star of order K: centre, then the x taps (dx = -K..-1, 1..K), the y taps,
-// the z taps -- first product rounded, then one FMA per tap.  xv/yv/zv(d)
-// return the sample at offset d on that axis.
-template <class T, int K, class P, class FX, class FY, class FZ>
-__device__ __forceinline__ T pipe_star_cell(const P& p, T c, FX xv, FY yv, FZ zv) {
-  T v = p.coef[cidx<K>(0, 0, 0)] * c;
-#pragma unroll
-  for (int d = -K; d <= K; ++d)
-    if (d != 0) v = fma_t(p.coef[cidx<K>(d, 0, 0)], xv(d), v);
-#pragma unroll
-  for (int d = -K; d <= K; ++d)
-    if (d != 0) v = fma_t(p.coef[cidx<K>(0, d, 0)], yv(d), v);
-#pragma unroll
-  for (int d = -K; d <= K; ++d)
-    if (d != 0) v = fma_t(p.coef[cidx<K>(0, 0, d)], zv(d), v);
-  return v;
-}
 
 // Box-family column partial j (dx = j-1) of order 1: the mask's taps of that
 // column, dz outer, dy inner, first product rounded.  sv(l, t) returns the

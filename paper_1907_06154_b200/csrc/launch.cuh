@@ -215,9 +215,8 @@ inline int halo_mode_3d() {
 }
 template <class T, int K, class Mask>
 constexpr bool halo_default_3d() {
-  return std::is_same<Mask, StarMask3<2>>::value ||
-         (sizeof(T) == 4 && (std::is_same<Mask, StarMask3<1>>::value ||
-                             std::is_same<Mask, PoissonMask3>::value));
+  return std::is_same<Mask, StarMask3<2>>::value || std::is_same<Mask, StarMask3<1>>::value ||
+         (sizeof(T) == 4 && std::is_same<Mask, PoissonMask3>::value);
 }
 
 // CTA order of the TMA kernels.  The hardware launches blockIdx.x fastest,

@@ -51,10 +51,29 @@ inline bool st2d_chain1() {
   return v;
 }
 
+// Orders >= 4 (2d17pt, 2d21pt, 2ds25pt, 2d121pt) take the register-row
+// engine (engine2d_conv.cuh) with the stencil's tap mask when the rows are
+// TMA-eligible; SSAM_B200_ST2D_REG=0 keeps them on the FMA engine.
+inline bool st2d_reg_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SSAM_B200_ST2D_REG");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 template <class T, int Q, int K, class Mask>
 cudaError_t st2d(const Engine2DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
   constexpr int QQ = st_q<T>(K);
+  if constexpr (K >= 4 && !std::is_same<T, long long>::value) {
+    if (st2d_reg_enabled()) {
+      const cudaError_t e = launch_conv2d_reg<T, M, Mask>(a.in, a.out, a.W, a.H, a.y_begin,
+                                                          a.y_end, a.coef, s, a.ring);
+      if (e != cudaErrorNotSupported) return e;
+      cudaGetLastError();
+    }
+  }
   if constexpr (K >= 4 && !std::is_same<T, long long>::value) {
     if (st2d_fma_enabled() && fma_eligible(a)) {
       constexpr int QW = QQ, RYW = 4;  // Q = 8 / RY = 2 measured no better (higher registers)

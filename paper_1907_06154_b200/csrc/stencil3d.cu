@@ -36,6 +36,15 @@ template <> struct Cfg3D<long long, 0> { static constexpr int RY = 4; };
 template <> struct Cfg3D<long long, 1> { static constexpr int RY = 4; };
 template <> struct Cfg3D<long long, 2> { static constexpr int RY = 2; };
 
+// SSAM_B200_STAR1_HALO=0 sends 3d7pt single sweeps to the pipeline kernel (TB = 1).
+inline bool star1_halo_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("SSAM_B200_STAR1_HALO");
+    return !e || std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 template <class T, int K, class Mask, int RY = Cfg3D<T, K>::RY>
 cudaError_t st3d(const Engine3DArgs<T>& a, cudaStream_t s) {
   constexpr int M = 2 * K + 1;
@@ -55,8 +64,17 @@ cudaError_t stencil3d_dispatch(const T* d_in, T* d_out, int nx, int ny, int nz, 
   if constexpr (SHAPES) {
     const Shape3D sh = classify3d(st.taps, k);
     if (pipe3d_enabled()) {  // the pipeline engine (engine3d_pipe.cuh)
-      if (k == 1 && sh == Shape3D::star)
+      if (k == 1 && sh == Shape3D::star) {
+        // single sweeps of the 7-point star: the halo-lane kernel runs the
+        // pipeline's per-cell chain (bit-identical to the fused launches)
+        // and streams faster at TB = 1 (profiles/r02/pipe_tb1_ab.txt:
+        // 2048^2 x 514 f32 776 vs 635-665 GCells/s, f64 382 vs 322-335)
+        constexpr int VQ = 16 / sizeof(T);
+        if (star1_halo_enabled() && halo_mode_3d() != 0 && nx % VQ == 0 && aligned16(d_in) &&
+            aligned16(d_out))
+          return st3d<T, 1, StarMask3<1>>(a, s);
         return pipe3d_star1<T>(d_in, d_out, nx, ny, nz, z_begin, z_end, 1, nz - 1, coef.data(), 1, s);
+      }
       if (k == 2 && sh == Shape3D::star)
         return pipe3d_star2<T>(d_in, d_out, nx, ny, nz, z_begin, z_end, 2, nz - 2, coef.data(), 1, s);
       if (k == 1)  // poisson, the 27-point box and any other order-1 tap set (dense)
