@@ -346,6 +346,17 @@ cudaMemPool_t engine_pool() {
   return g_pools[dev];
 }
 
+}  // namespace
+
+namespace ssam_b200 {
+cudaError_t engine_alloc(void** p, std::size_t bytes, cudaStream_t s) {
+  cudaMemPool_t pool = engine_pool();
+  return pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
+}
+}  // namespace ssam_b200
+
+namespace {
+
 struct DevBuf {
   void* p = nullptr;
   cudaStream_t s;

@@ -71,9 +71,9 @@ namespace {
 template <class T>
 cudaError_t upload_taps(const std::vector<int>& offs, const std::vector<T>& c, int** d_offs,
                         T** d_c, cudaStream_t s) {
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(d_offs), offs.size() * sizeof(int), s);
+  cudaError_t e = engine_alloc(reinterpret_cast<void**>(d_offs), offs.size() * sizeof(int), s);
   if (e != cudaSuccess) return e;
-  e = cudaMallocAsync(reinterpret_cast<void**>(d_c), c.size() * sizeof(T), s);
+  e = engine_alloc(reinterpret_cast<void**>(d_c), c.size() * sizeof(T), s);
   if (e != cudaSuccess) return e;
   e = cudaMemcpyAsync(*d_offs, offs.data(), offs.size() * sizeof(int), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return e;

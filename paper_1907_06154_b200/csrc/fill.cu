@@ -85,7 +85,7 @@ __global__ void max_err_kernel(const T* __restrict__ a, const T* __restrict__ b,
 cudaError_t max_rel_err(int dtype, const void* d_a, const void* d_b, size_t count, double* h_rel,
                         double* h_abs, cudaStream_t s) {
   unsigned long long* d_out = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&d_out), 16, s);
+  cudaError_t e = engine_alloc(reinterpret_cast<void**>(&d_out), 16, s);
   if (e != cudaSuccess) return e;
   cudaMemsetAsync(d_out, 0, 16, s);
   const int blocks = static_cast<int>(std::min<size_t>((count + 255) / 256 + 1, 148 * 16));

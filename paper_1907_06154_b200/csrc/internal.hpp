@@ -132,6 +132,10 @@ cudaError_t scan_device(const T* d_in, T* d_out, size_t n, cudaStream_t s);
 cudaError_t measure_latency(double* t, cudaStream_t s);
 
 // ---- utilities --------------------------------------------------------------
+// Stream-ordered scratch from the engine's private per-device pool (freed
+// blocks stay cached; the device's default pool is never touched).  Free
+// with cudaFreeAsync.
+cudaError_t engine_alloc(void** p, std::size_t bytes, cudaStream_t s);
 cudaError_t fill_random(int dtype, void* d, std::size_t count, std::uint64_t seed,
                         std::uint64_t first, cudaStream_t s);
 // max |a-b| / max(1,|b|) and max |a-b| over count elements, into host doubles.

@@ -121,6 +121,8 @@ cudaError_t multi_stencil(const T* h_in, T* h_out, int nx, int ny, int nz, const
     SSAM_TRY(cudaEventCreateWithFlags(&s.bnd, cudaEventDisableTiming));
     SSAM_TRY(cudaEventCreateWithFlags(&s.cp, cudaEventDisableTiming));
     const size_t bytes = static_cast<size_t>(s.nl) * pe * sizeof(T);
+    // plain allocations: peers copy into them (pool memory would need
+    // per-peer access descriptors)
     SSAM_TRY(cudaMalloc(&s.buf[0], bytes));
     SSAM_TRY(cudaMalloc(&s.buf[1], bytes));
   }

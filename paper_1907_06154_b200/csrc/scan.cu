@@ -208,7 +208,7 @@ cudaError_t scan_impl(const T* d_in, T* d_out, size_t n, cudaStream_t s) {
   const size_t tiles = (n + TILE - 1) / TILE;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
   T* scratch = nullptr;  // tile sums, then tile prefixes (stream-ordered pool)
-  cudaError_t e = cudaMallocAsync(&scratch, 2 * tiles * sizeof(T), s);
+  cudaError_t e = engine_alloc(reinterpret_cast<void**>(&scratch), 2 * tiles * sizeof(T), s);
   if (e != cudaSuccess) return e;
   const unsigned g = static_cast<unsigned>(tiles);
   scan_reduce_kernel<T><<<g, kScanThreads, 0, s>>>(d_in, n, scratch);
