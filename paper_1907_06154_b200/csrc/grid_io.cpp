@@ -99,6 +99,12 @@ int ssam_b200_sgrd_read(const char* path, int dtype, int rank, int* dims, void* 
   if (r != rank) return set_error(SSAM_ERR_RUNTIME, "grid io: rank mismatch");
   if (d != dtype) return set_error(SSAM_ERR_RUNTIME, "grid io: scalar type mismatch");
   if (dims) std::memcpy(dims, dm, sizeof dm);
+  // read_grid2d / read_grid3d construct the grid before the payload, and the
+  // Grid2D / Grid3D constructors reject empty dimensions (grid.hpp:20, :38)
+  if (rank == 2 && (dm[0] < 1 || dm[1] < 1))
+    return set_error(SSAM_ERR_INVALID_ARGUMENT, "grid2d: dimensions must be >= 1");
+  if (rank == 3 && (dm[0] < 1 || dm[1] < 1 || dm[2] < 1))
+    return set_error(SSAM_ERR_INVALID_ARGUMENT, "grid3d: dimensions must be >= 1");
   const size_t count = size_t(dm[0]) * (rank >= 2 ? dm[1] : 1) * (rank >= 3 ? dm[2] : 1);
   if (!dst) return count == 0 ? SSAM_OK : set_error(SSAM_ERR_INVALID_ARGUMENT, "grid io: null buffer");
   if (count > capacity)
@@ -137,13 +143,15 @@ int ssam_b200_sgrd_write(const char* path, int dtype, int rank, const int* dims,
   if (dtype < 0 || dtype > 2) return set_error(SSAM_ERR_INVALID_ARGUMENT, "unknown dtype");
   if (rank < 1 || rank > 3 || !dims) return set_error(SSAM_ERR_INVALID_ARGUMENT, "grid io: bad rank");
   int dm[3] = {dims[0], rank >= 2 ? dims[1] : 1, rank >= 3 ? dims[2] : 1};
+  // write_grid_file (grid_io.hpp:129-134) opens -- and truncates -- the file
+  // first, then write_header rejects oversize dimensions (:43-46)
+  File f(path, "wb");
+  if (!f.f) return set_error(SSAM_ERR_RUNTIME, std::string("grid io: cannot open ") + (path ? path : "") + " for writing");
   for (int i = 0; i < 3; ++i)
     if (dm[i] > 0xffff)
       return set_error(SSAM_ERR_INVALID_ARGUMENT, "grid io: dimension exceeds format limit (65535)");
   for (int i = 0; i < 3; ++i)
     if (dm[i] < 0) return set_error(SSAM_ERR_INVALID_ARGUMENT, "grid io: negative dimension");
-  File f(path, "wb");
-  if (!f.f) return set_error(SSAM_ERR_RUNTIME, std::string("grid io: cannot open ") + (path ? path : "") + " for writing");
   unsigned char h[16] = {'S', 'G', 'R', 'D', 1, static_cast<unsigned char>(rank),
                          static_cast<unsigned char>(scalar_code(dtype)), 0};
   for (int i = 0; i < 3; ++i) {

@@ -80,3 +80,14 @@ def test_multi_rejects_bad_device(cuda_lib):
         cuda_lib.stencil_multi(g, st, [0, 4096])
     with pytest.raises(cuda_lib.InvalidArgument):
         cuda_lib.stencil_multi(g, st, [])
+
+
+def test_multi_large_slabs(cuda_lib):
+    """A larger grid (2048 x 512 x 256 f32, 4 slabs, 12 sweeps: fused pairs
+    with the ghost exchange every round) through the device-set path equals
+    the one-device call bit for bit."""
+    st = cuda_lib.convert_stencil(cuda_lib.make_benchmark_stencil("3d7pt"), np.float32)
+    g = cuda_lib.random_grid3d(2048, 512, 256, 7, np.float32)
+    one = cuda_lib.stencil3d(g, st, None, 12)
+    got, used = cuda_lib.stencil_multi(g, st, [0, 0, 0, 0], None, 12)
+    assert used == 4 and np.array_equal(got, one)

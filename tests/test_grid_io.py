@@ -73,6 +73,25 @@ def test_error_contract(lib, orc, ref, tmp):
     with pytest.raises(lib.InvalidArgument):
         lib.write_grid(tmp("big.sgrd"), big)
     assert ref.sgrd_write(tmp("bigr.sgrd"), big) == 1
+    # both open (and truncate) the file before rejecting the dimensions
+    assert os.path.exists(tmp("big.sgrd")) and os.path.getsize(tmp("big.sgrd")) == 0
+    assert os.path.exists(tmp("bigr.sgrd")) and os.path.getsize(tmp("bigr.sgrd")) == 0
+    # an unopenable path with oversize dims: the open failure wins (runtime_error)
+    with pytest.raises(lib.GridIOError):
+        lib.write_grid(tmp("no/such/dir/big.sgrd"), big)
+    assert ref.sgrd_write(tmp("no/such/dir/bigr.sgrd"), big) == 3
+    # a header with an empty dimension: Grid2D / Grid3D reject it (invalid_argument)
+    for rank, dt, shape in ((2, np.float64, (4, 3)), (3, np.float64, (2, 3, 4))):
+        src = tmp(f"z{rank}.sgrd")
+        lib.write_grid(src, orc.random_grid(shape, dt, 1))
+        blob = bytearray(open(src, "rb").read())
+        blob[8:10] = b"\x00\x00"            # dims[0] = 0
+        bad = tmp(f"zero{rank}.sgrd")
+        open(bad, "wb").write(bytes(blob[:16]))
+        read = lib.read_grid2d if rank == 2 else lib.read_grid3d
+        with pytest.raises(lib.InvalidArgument):
+            read(bad, dt)
+        assert ref.sgrd_read(bad, dt, rank)[0] == 1
 
 
 @pytest.mark.gpu
