@@ -63,18 +63,33 @@ struct PipeGeom {
   static constexpr bool STAR = Sh::STAR;
   static constexpr int Q = 16 / static_cast<int>(sizeof(T));
   static constexpr int BW = 32 * Q;  // strip / box / slot row width
-  static constexpr int ROWS = 16;
+#ifndef SSAM_P2_ROWS
+#define SSAM_P2_ROWS 16
+#endif
+  static constexpr int ROWS = (TB == 2 && K == 1) ? SSAM_P2_ROWS : 16;
+// Tb = 2 order-1 star: 6 stage-1 warps x 3 rows and 6 stage-2 warps x 3
+// rows (18 >= 16).  ncu's stall sampling of the 6x3 / 4x4 split had stage 1
+// waiting on the intermediate ring's EMPTY barriers (26% of all samples):
+// stage 2, which also stores to HBM, was the slower stage.  Balanced:
+// 2048^2 x 514 f32 1390 -> 1427, f64 512^3 569 -> 667 GCells/s
+// (profiles/r02/pipe_stage_ab.txt); 2 CTAs / SM still fit (67 registers).
+#ifndef SSAM_P2_SY1
+#define SSAM_P2_SY1 6
+#define SSAM_P2_RY1 3
+#define SSAM_P2_SY2 6
+#define SSAM_P2_RY2 3
+#endif
   static constexpr int sy(int s) {
     if (K == 2) return TB == 1 ? 8 : (s == 1 ? 10 : 8);
     return TB == 1 ? 4
-         : TB == 2 ? (s == 1 ? 6 : 4)
+         : TB == 2 ? (s == 1 ? SSAM_P2_SY1 : SSAM_P2_SY2)
          : TB == 3 ? (s == 1 ? 5 : s == 2 ? 6 : 4)
                    : (s == 1 ? 4 : s == 2 ? 5 : s == 3 ? 6 : 4);
   }
   static constexpr int ry(int s) {
     if (K == 2) return 2;
     return TB == 1 ? 4
-         : TB == 2 ? (s == 1 ? 3 : 4)
+         : TB == 2 ? (s == 1 ? SSAM_P2_RY1 : SSAM_P2_RY2)
          : TB == 3 ? (s == 1 ? 4 : s == 2 ? 3 : 4)
                    : (s == 1 ? 6 : s == 2 ? 4 : s == 3 ? 3 : 4);
   }
@@ -124,7 +139,8 @@ struct PipeGeom {
   // when fused)
   static constexpr int MINB = !STAR && TB > 1 ? 1
                             : THREADS <= 160 ? 3
-                            : (THREADS <= 352 ? (TB == 2 ? SSAM_STAR_MINB2 : 2) : 1);
+                            : (THREADS <= 352 ? (TB == 2 ? SSAM_STAR_MINB2 : 2)
+                                              : (TB == 2 && K == 1 && THREADS <= 512 ? SSAM_STAR_MINB2 : 1));
   static constexpr int CAP = (2 * K + 1) * (2 * K + 1) * (2 * K + 1);
   static_assert(IN_ROWS <= 256, "TMA box rows");
   static_assert(K <= Q, "x halo within one neighbour lane");
