@@ -507,7 +507,8 @@ def e2e_run(args, slab, st, world, rank, tb, ref_result):
     if world == 1:
         shape = (NZ_PER_GPU, NY, NX)
         host_in = torch.empty(shape, dtype=torch.float32, pin_memory=True)
-        outs = [torch.empty(shape, dtype=torch.float32, pin_memory=True) for _ in range(2)]
+        depth = 3  # grids in flight: H2D of k+1, sweeps of k, D2H of k-1 (2 x 8 GiB each)
+        outs = [torch.empty(shape, dtype=torch.float32, pin_memory=True) for _ in range(depth)]
         tmp = torch.empty(shape, dtype=torch.float32, device="cuda")
         dev.fill_random(tmp, 0)
         host_in.copy_(tmp)
@@ -535,16 +536,16 @@ def e2e_run(args, slab, st, world, rank, tb, ref_result):
         dt1 = time.perf_counter() - t0
 
         def batch(n):
-            ssam.stencil_batch([host_in] * n, [outs[i % 2] for i in range(n)], st, args.iters,
-                               depth=2)
+            ssam.stencil_batch([host_in] * n, [outs[i % depth] for i in range(n)], st, args.iters,
+                               depth=depth)
 
-        batch(2)  # warm-up of the batch buffers
+        batch(depth)  # warm-up of the batch buffers
         t0 = time.perf_counter()
         batch(steps)
         dtb = time.perf_counter() - t0
         same_b = None
         if ref_result is not None:
-            chk = outs[(steps - 1) % 2].to("cuda", non_blocking=False)
+            chk = outs[(steps - 1) % depth].to("cuda", non_blocking=False)
             same_b = bool(torch.equal(chk, ref_result))
             del chk
         cells = NX * NY * NZ_PER_GPU * args.iters * steps
@@ -721,7 +722,7 @@ def main():
     ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
                     help="N > 1 halo transport: NCCL send/recv, or the sweep kernel's own "
                          "stores into the neighbours' buffers (CUDA IPC / NVLink P2P)")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-suite", action="store_true")

@@ -112,7 +112,9 @@ struct PipeGeom {
 #ifndef SSAM_STAR_DZ1
 #define SSAM_STAR_DZ1 SSAM_STAR_DZ
 #endif
-  static constexpr int DZW = TB == 1 ? SSAM_STAR_DZ1 : SSAM_STAR_DZ;
+  // single sweeps of the order-2 star keep 8 planes in flight (3d13pt
+  // 512^3 f32 612 -> 656, f64 360 -> 370; profiles/r02/dz1_ab.txt)
+  static constexpr int DZW = TB == 1 ? (K == 2 ? 8 : SSAM_STAR_DZ1) : SSAM_STAR_DZ;
   static constexpr int DZ = DZW > 2 * K + 2 ? DZW : 2 * K + 2;
   static constexpr int DI = SSAM_STAR_DI > 2 * K + 1 ? SSAM_STAR_DI : 2 * K + 1;
   static constexpr int cmax(int a, int b) { return a > b ? a : b; }

@@ -7,4 +7,5 @@ for sp in ${SPECS}; do
   python tools/ncu_summary.py /tmp/$t.ncu-rep > gpurun_out/$t.sum.txt
   ncu -i /tmp/$t.ncu-rep --page source --csv --print-source sass > /tmp/$t.sass.csv 2>/dev/null
   python tools/sass_mix.py /tmp/$t.sass.csv > gpurun_out/$t.mix.txt
+  [ -n "$KEEP_SASS" ] && cp /tmp/$t.sass.csv gpurun_out/
 done
