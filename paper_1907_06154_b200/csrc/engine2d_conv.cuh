@@ -246,7 +246,10 @@ struct ConvRegCfg {
 #ifndef SSAM_CONVREG_Q32
 #define SSAM_CONVREG_Q32 4
 #endif
-  static constexpr int Q = sizeof(T) == 4 ? SSAM_CONVREG_Q32 : 2;
+#ifndef SSAM_CONVREG_Q64
+#define SSAM_CONVREG_Q64 2
+#endif
+  static constexpr int Q = sizeof(T) == 4 ? SSAM_CONVREG_Q32 : SSAM_CONVREG_Q64;
 #ifndef SSAM_CONVREG_RY
 #define SSAM_CONVREG_RY 4
 #endif

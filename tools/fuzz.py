@@ -88,6 +88,13 @@ while time.time() < t_end:
             got = ssam.stencil3d(g, st, ssam.KernelConfig(p=2, b=128 if k < 2 else 256), iters)
             want = orc.stencil3d(g, offs, cf, k, iters)
         note(fam, dt, max_rel_err(got, want), (st.name, shape, iters))
+        if rng.random() < 0.3:
+            # the device-set path (slabs sharing device 0) must equal it bit for bit
+            ndev = int(rng.integers(2, 5))
+            cfg = ssam.KernelConfig() if dims == 2 else ssam.KernelConfig(p=2, b=128 if k < 2 else 256)
+            multi, _ = ssam.stencil_multi(g, st, [0] * ndev, cfg, iters)
+            note(fam + "_multi", dt, 0.0 if np.array_equal(multi, got) else float("inf"),
+                 (st.name, shape, iters, ndev))
     elif fam == "conv1d":
         m = int(rng.integers(1, 33))
         nlen = int(rng.integers(32, 20000))
