@@ -63,22 +63,24 @@ struct PipeGeom {
   static constexpr bool STAR = Sh::STAR;
   static constexpr int Q = 16 / static_cast<int>(sizeof(T));
   static constexpr int BW = 32 * Q;  // strip / box / slot row width
+  // Tb = 2 order-1 star, stage geometry per element type (profiles/r02/
+  // pipe_stage_ab.txt, sustained_ab2.txt).  Round 1's 6 x 3 / 4 x 4 split
+  // left stage 1 waiting on the intermediate ring's EMPTY barriers (26% of
+  // ncu's stall samples): stage 2, which also stores to HBM, was the slower
+  // stage.  fp32 (the headline): 18 output rows, stage 1 5 warps x 4 rows
+  // (20 = 18 + 2 halo), stage 2 6 x 3 -- no idle rows; under the bench's
+  // sustained, power-capped load 1203 -> 1295 GCells/s (6 x 3 / 6 x 3: 1247).
+  // fp64: 16 rows, 6 x 3 / 6 x 3 (2048^2 x 258 660 -> 720 in short runs).
 #ifndef SSAM_P2_ROWS
-#define SSAM_P2_ROWS 16
+#define SSAM_P2_ROWS (sizeof(T) == 4 ? 18 : 16)
 #endif
-  static constexpr int ROWS = (TB == 2 && K == 1) ? SSAM_P2_ROWS : 16;
-// Tb = 2 order-1 star: 6 stage-1 warps x 3 rows and 6 stage-2 warps x 3
-// rows (18 >= 16).  ncu's stall sampling of the 6x3 / 4x4 split had stage 1
-// waiting on the intermediate ring's EMPTY barriers (26% of all samples):
-// stage 2, which also stores to HBM, was the slower stage.  Balanced:
-// 2048^2 x 514 f32 1390 -> 1427, f64 512^3 569 -> 667 GCells/s
-// (profiles/r02/pipe_stage_ab.txt); 2 CTAs / SM still fit (67 registers).
 #ifndef SSAM_P2_SY1
-#define SSAM_P2_SY1 6
-#define SSAM_P2_RY1 3
+#define SSAM_P2_SY1 (sizeof(T) == 4 ? 5 : 6)
+#define SSAM_P2_RY1 (sizeof(T) == 4 ? 4 : 3)
 #define SSAM_P2_SY2 6
 #define SSAM_P2_RY2 3
 #endif
+  static constexpr int ROWS = (TB == 2 && K == 1) ? static_cast<int>(SSAM_P2_ROWS) : 16;
   static constexpr int sy(int s) {
     if (K == 2) return TB == 1 ? 8 : (s == 1 ? 10 : 8);
     return TB == 1 ? 4
