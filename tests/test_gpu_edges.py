@@ -92,3 +92,38 @@ def test_public_api_fuzz(cuda_lib):
     p = subprocess.run([sys.executable, "tools/fuzz.py", "15"], cwd=root, capture_output=True,
                        text=True, timeout=600, env=dict(os.environ, FUZZ_SEED="11"))
     assert "FUZZ PASS" in p.stdout, p.stdout[-3000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("name,tb", [("3d7pt", 2), ("3d7pt", 3), ("3d13pt", 2), ("poisson", 2)])
+def test_fused_ranges_outside_the_buffer(cuda_lib, name, tb):
+    """ssam_b200_stencil3d_tb with output planes and ring bounds that lie
+    outside the buffer (a slab passes its local ring bounds): the launch is
+    clamped to the buffer's interior -- nothing outside the buffer is written
+    (guard planes around it stay intact) and the result equals the in-range
+    call away from the buffer's ends (launch_tb3d clamped only to
+    the ring bounds)."""
+    import torch
+    from paper_1907_06154_b200 import device as dev
+    st = cuda_lib.convert_stencil(cuda_lib.make_benchmark_stencil(name), np.float32)
+    k = st.order
+    nz, ny, nx = 24, 40, 128
+    guard = 8
+    big_in = torch.full((nz + 2 * guard, ny, nx), 7.0, dtype=torch.float32, device="cuda")
+    a = big_in[guard:guard + nz]
+    dev.fill_random(a, 3)
+    big_out = torch.full_like(big_in, -5.0)
+    b = big_out[guard:guard + nz]
+    b.copy_(a)
+    ref = a.clone()
+    dev.stencil3d_tb(a, ref, st, tb)  # the in-range call
+    # outputs requested far past both ends, ring bounds outside the buffer
+    dev.stencil3d_tb(a, b, st, tb, -50, nz + 50, -40, nz + 40)
+    assert torch.equal(big_out[:guard], torch.full_like(big_out[:guard], -5.0))
+    assert torch.equal(big_out[guard + nz:], torch.full_like(big_out[guard + nz:], -5.0))
+    # outputs are clamped to the buffer's interior [k, nz - k): its first /
+    # last k planes are never written
+    assert torch.equal(b[:k], a[:k]) and torch.equal(b[nz - k:], a[nz - k:])
+    # away from the buffer's ends (beyond the fused cone) the declared ring
+    # makes no difference: equal to the in-range call bit for bit
+    c = 2 * k * tb
+    assert torch.equal(b[c:nz - c], ref[c:nz - c])
