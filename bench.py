@@ -722,7 +722,7 @@ def main():
     ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
                     help="N > 1 halo transport: NCCL send/recv, or the sweep kernel's own "
                          "stores into the neighbours' buffers (CUDA IPC / NVLink P2P)")
-    ap.add_argument("--e2e-steps", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-suite", action="store_true")

@@ -143,9 +143,10 @@ template <class T, int Q, int N>
 cudaError_t conv_rt(const Engine2DArgs<T>& a, cudaStream_t s) {
   return launch_ssam2d<T, Q, N, 0, DenseMask, pf_rows(N), 20 * N>(a, s);
 }
-// K = 6..15 take the register-row engine (engine2d_conv.cuh; 16+ lose to
-// the two-level chain engine, profiles/r02/conv_reg_big_ab.txt) unless
-// SSAM_B200_CONV_REG=0.
+// K = 5..15 take the register-row engine (engine2d_conv.cuh) unless
+// SSAM_B200_CONV_REG=0: 5x5 536 -> 602-622 GCells/s (3x3 / 4x4 gain nothing,
+// profiles/r02/conv_small_ab.txt); 16+ lose to the two-level chain engine
+// (profiles/r02/conv_reg_big_ab.txt).
 inline bool conv_reg_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("SSAM_B200_CONV_REG");
@@ -154,7 +155,7 @@ inline bool conv_reg_enabled() {
   return v;
 }
 #ifndef SSAM_CONV_REG_MIN
-#define SSAM_CONV_REG_MIN 6
+#define SSAM_CONV_REG_MIN 5
 #endif
 #ifndef SSAM_CONV_REG_MAX
 #define SSAM_CONV_REG_MAX 15

@@ -1,5 +1,5 @@
-// engine2d_conv.cuh -- the FMA-bound conv2d engine for mid-size square
-// filters (K = 6..11), sm_100a.
+// engine2d_conv.cuh -- the register-row engine: conv2d with square filters
+// K = 5..15 and the 2D stencils of order 4..6 (with their tap mask), sm_100a.
 //
 // Reference: ssam::conv2d (proj/include/ssam/kernels.hpp:189-225), the true
 // convolution out(x,y) = sum_{s,t} in(x+ax-s, y+ay-t) * w[s*n+t]
@@ -7,7 +7,7 @@
 //     out(x, y) = sum_{j,t} coef[j*K+t] * in(x + j - L, y + t - U)
 // with coef[j][t] = w[(K-1-j)*K + (K-1-t)] (conv_coef, kernels.hpp:90).
 //
-// Why not the shuffle chain here: at K >= 6 the conv is FMA-bound (2K^2
+// Why not the shuffle chain here: from K ~ 6 the conv is FMA-bound (2K^2
 // flop per output), and in the systolic chain every
 // column step costs a SHFL plus Q-1 register moves per output vector, the
 // chain's first/last lanes hold no valid output, and the window shift adds
@@ -22,10 +22,10 @@
 // are FFMAs with the weights as constant-bank operands, every lane's Q
 // columns are outputs, and no shuffles are needed.
 //
-// Per output the sum is ONE FMA chain, rows t outer, columns j inner
-// (a fixed order, so results are deterministic; fp32 within 1e-5 of the
-// double-accumulated oracle for K <= 11 -- SURVEY §8(c) caveat 1 applies
-// only from 17x17).
+// Per output the sum is ONE FMA chain, rows t outer, columns j inner (a
+// fixed order, so results are deterministic; fp32 within 1e-5 of the
+// double-accumulated oracle); from 12x12 each input row's K taps are summed
+// first and the row partials added (two-level, SURVEY §8(c) caveat 1).
 #pragma once
 
 #include <type_traits>
