@@ -256,7 +256,13 @@ struct ConvRegCfg {
 #ifndef SSAM_CONVREG_RY_BIG
 #define SSAM_CONVREG_RY_BIG 2
 #endif
-  static constexpr int RY = mask_tap_count<Mask, K>() <= 121 ? SSAM_CONVREG_RY : SSAM_CONVREG_RY_BIG;
+#ifndef SSAM_CONVREG_RY_STAR
+#define SSAM_CONVREG_RY_STAR 6
+#endif
+  // star stencils: 6 rows per pass (2ds25pt f32 609 -> 652 GCells/s, 2d21pt
+  // / 2d17pt +3%; dense filters keep 4 -- profiles/r02/st2d_ry_ab.txt)
+  static constexpr int RY = IsStar2D<Mask>::value ? SSAM_CONVREG_RY_STAR
+                          : mask_tap_count<Mask, K>() <= 121 ? SSAM_CONVREG_RY : SSAM_CONVREG_RY_BIG;
   static constexpr int RB = RY;
   // rows kept for the window (K - 1) + one pass in flight + prefetch
   static constexpr int D = (K - 1 + RB - 1) / RB + 3;
