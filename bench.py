@@ -25,7 +25,7 @@ each GPU always owns 2048 x 2048 x 512 cells.
           sweep 3x3..20x20, 2D stencils x100 sweeps, 3D stencils at 512^3),
           rank 0 at N=1.
   cpu_baseline  the reference's own CPU path (oracle/_ref, ssam::stencil3d)
-          on bounded samples of the same workload: threads=0 and threads=1,
+          on bounded samples of the same workload: every host thread and threads=1,
           best of 3 each.
 
 --impl reference times that reference CPU path alone (rank 0; other ranks
@@ -135,7 +135,7 @@ def cpu_model() -> str:
     return "unknown"
 
 
-CPU_BLOCK_NZ = 16     # planes of the threads=0 sample block (14 of them updated per sweep)
+CPU_BLOCK_NZ = 16     # planes of the all-threads sample block (14 of them updated per sweep)
 CPU_BLOCK1_NZ = 4     # planes of the threads=1 sample block (2 updated)
 
 
@@ -150,6 +150,16 @@ def _ref_block(nz: int):
     return ref, st, g, st["coeffs"].astype(np.float32)
 
 
+def host_threads() -> int:
+    """Every host thread, passed to the reference as KernelConfig::threads
+    (kernels.hpp:42-45 num_threads): torchrun exports OMP_NUM_THREADS=1,
+    which would otherwise pin threads=0 to one core."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
 def _ref_sweep_seconds(ref, st, g, cf, threads: int) -> float:
     t0 = time.perf_counter()
     rc, _, _ = ref.stencil3d(g, st["offsets"], cf, st["order"], 1, p=2, b=128, threads=threads)
@@ -160,21 +170,22 @@ def _ref_sweep_seconds(ref, st, g, cf, threads: int) -> float:
 def reference_sample(seconds: float = 10.0):
     """The reference's own CPU SSAM path (ssam::stencil3d from oracle/_ref,
     -O3 -fopenmp) on bounded samples of the workload, best of 3 as
-    proj/tools/threads_bench.cpp:25-35 times it: threads=0 (every host
-    thread) on a 2048x2048x16 block and threads=1 on a 2048x2048x4 block.
+    proj/tools/threads_bench.cpp:25-35 times it: every host thread (threads = the
+    host thread count) on a 2048x2048x16 block and threads=1 on a 2048x2048x4 block.
     The rate counts the cells of the planes a sweep advances (nz - 2 planes
     of 2048 x 2048), the same W*H-per-plane convention as the GPU value."""
     ref, st, g, cf = _ref_block(CPU_BLOCK_NZ)
     upd = (CPU_BLOCK_NZ - 2) * NX * NY
-    best = min(_ref_sweep_seconds(ref, st, g, cf, 0) for _ in range(3))
+    nall = host_threads()
+    best = min(_ref_sweep_seconds(ref, st, g, cf, nall) for _ in range(3))
     ref1, st1, g1, cf1 = _ref_block(CPU_BLOCK1_NZ)
     upd1 = (CPU_BLOCK1_NZ - 2) * NX * NY
     best1 = min(_ref_sweep_seconds(ref1, st1, g1, cf1, 1) for _ in range(3))
     return {
-        "value": round(upd / best / 1e9, 6), "unit": "GCells/s", "cores": ref.max_threads(),
+        "value": round(upd / best / 1e9, 6), "unit": "GCells/s", "cores": nall,
         "kind": "reference",
         "sample": (f"best of 3 single sweeps of ssam::stencil3d<float> 3d7pt (oracle/_ref, "
-                   f"threads=0 = {ref.max_threads()} threads) on global planes 0..{CPU_BLOCK_NZ - 1} "
+                   f"threads={nall}, every host thread) on global planes 0..{CPU_BLOCK_NZ - 1} "
                    f"of the seed-0 grid ({NX}x{NY}x{CPU_BLOCK_NZ}; {CPU_BLOCK_NZ - 2} planes "
                    f"updated per sweep, counted as {CPU_BLOCK_NZ - 2}*{NX}*{NY} cells)"),
         "threads1": {"value": round(upd1 / best1 / 1e9, 6), "unit": "GCells/s", "cores": 1,
@@ -190,15 +201,16 @@ def run_reference_arm(args, rank: int, world: int):
         return
     ref, st, g, cf = _ref_block(CPU_BLOCK_NZ)
     upd = (CPU_BLOCK_NZ - 2) * NX * NY
+    nall = host_threads()
     for _ in range(args.warmup):
-        _ref_sweep_seconds(ref, st, g, cf, 0)
+        _ref_sweep_seconds(ref, st, g, cf, nall)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        _ref_sweep_seconds(ref, st, g, cf, 0)
+        _ref_sweep_seconds(ref, st, g, cf, nall)
     dt = time.perf_counter() - t0
     value = upd * args.steps / dt / 1e9
-    sample = (f"each step: 1 sweep of ssam::stencil3d<float> 3d7pt (oracle/_ref, threads=0 = "
-              f"{ref.max_threads()} threads) on global planes 0..{CPU_BLOCK_NZ - 1} of the seed-0 "
+    sample = (f"each step: 1 sweep of ssam::stencil3d<float> 3d7pt (oracle/_ref, threads={nall}, "
+              f"every host thread) on global planes 0..{CPU_BLOCK_NZ - 1} of the seed-0 "
               f"workload grid ({CPU_BLOCK_NZ - 2} planes of {NX}x{NY} updated and counted)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": "GCells/s",
@@ -207,7 +219,7 @@ def run_reference_arm(args, rank: int, world: int):
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(world, args),
         "cpu_baseline": {"value": round(value, 6), "unit": "GCells/s",
-                         "cores": ref.max_threads(), "kind": "reference", "sample": sample,
+                         "cores": nall, "kind": "reference", "sample": sample,
                          "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": round(value, 6), "unit": "GCells/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
