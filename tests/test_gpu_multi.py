@@ -25,7 +25,8 @@ def test_multi_3d_bit_identical(cuda_lib, orc, name, dt):
     offs = [t.offset for t in st.taps]
     cf = np.asarray([t.coeff for t in st.taps], dt)
     for (nx, ny, nz), iters, ndev in (((64, 40, 48), 5, 2), ((128, 33, 61), 7, 3),
-                                      ((64, 16, 97), 4, 4), ((36, 20, 30), 3, 2)):
+                                      ((64, 16, 97), 4, 4), ((36, 20, 30), 3, 2),
+                                      ((33, 21, 40), 5, 3)):  # unaligned rows: direct kernels
         g = orc.random_grid((nz, ny, nx), dt, 11)
         one = cuda_lib.stencil3d(g, st, None, iters)
         got, used = cuda_lib.stencil_multi(g, st, [0] * ndev, None, iters)
