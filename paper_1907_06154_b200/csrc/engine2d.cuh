@@ -40,6 +40,8 @@
 
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ssam_b200 {
@@ -80,19 +82,9 @@ struct StarMask2D {
 template <class Mask> struct IsStar2D { static constexpr bool value = false; };
 template <int K> struct IsStar2D<StarMask2D<K>> { static constexpr bool value = true; };
 
-// One output row of an order-K star as ONE chain per output -- the
-// reference simulator's stage order (kernels.hpp:111-159: taps bucketed by
-// column, rows ascending, one MAD per tap into the shifted partial sum):
-//   left  chain  j = 0..K      (dx = -K..0) flows up:   first tap rounded
-//                               product, then shift + FMA per tap;
-//   right chain  j = 2K..K+1   (dx = K..1) flows down the same way;
-//   out = left + right          (one rounded add).
-// Window row t (dy = t - K) is buf[(rot + t) % NB]; coef(j, t) returns the
-// tap's coefficient.  Written with mul_t / fma_t / add_t only (no
-// contraction freedom), so the single-sweep engines and every temporal-
-// blocking stage produce bit-identical rows.
+// Column-chain form of the star row (left chain up, right chain down).
 template <class T, int Q, int K, int NB, class CF>
-__device__ __forceinline__ void star_row_chain(const T (&buf)[NB][Q], int rot, CF coef,
+__device__ __forceinline__ void star_row_colchain(const T (&buf)[NB][Q], int rot, CF coef,
                                                T (&acc)[Q]) {
   constexpr int NR = 2 * K + 1;
   {
@@ -132,6 +124,48 @@ __device__ __forceinline__ void star_row_chain(const T (&buf)[NB][Q], int rot, C
     shift_down1<T, Q>(accr);
 #pragma unroll
     for (int q = 0; q < Q; ++q) acc[q] = add_t(acc[q], accr[q]);
+  }
+}
+
+// One output row of an order-K star as ONE FMA chain per output: the
+// centre tap's rounded product, then the x taps (dx = -K..-1, 1..K), then
+// the y taps (dy = -K..-1, 1..K) -- the 3D pipeline's order
+// (pipe_star_cell).  The x neighbours are the centre row's own values: a
+// lane's Q columns plus K columns shuffled in from each neighbour lane (K
+// SHFL up, K down per row), so every tap is one FFMA (2d5pt: 1 FMUL + 4
+// FFMA per cell).  Window row t (dy = t - K) is buf[(rot + t) % NB];
+// coef(j, t) returns the tap's coefficient.  Written with mul_t / fma_t only
+// (no contraction freedom), so the single-sweep engines and every
+// temporal-blocking stage produce bit-identical rows.  (fp64, int64: the
+// column-chain order above.)
+template <class T, int Q, int K, int NB, class CF>
+__device__ __forceinline__ void star_row_chain(const T (&buf)[NB][Q], int rot, CF coef,
+                                               T (&acc)[Q]) {
+  // fp32: 2d5pt Tb 4 1750 -> 1935, 2d9pt Tb 2 1135 -> 1182 GCells/s; fp64
+  // measured 4% slower at 2d5pt Tb 4 and keeps the column chain
+  // (profiles/r02/star2d_chain_ab.txt)
+  if constexpr (K >= 1 && K <= Q && std::is_same<T, float>::value) {
+    const T(&cr)[Q] = buf[(rot + K) % NB];
+    T lft[K], rgt[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      lft[i] = shfl_up(cr[Q - K + i], 1);
+      rgt[i] = __shfl_down_sync(kFull, cr[i], 1);
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      auto xs = [&](int qq) { return qq < 0 ? lft[K + qq] : (qq >= Q ? rgt[qq - Q] : cr[qq]); };
+      T v = mul_t(coef(K, K), cr[q]);
+#pragma unroll
+      for (int d = -K; d <= K; ++d)
+        if (d != 0) v = fma_t(coef(K + d, K), xs(q + d), v);
+#pragma unroll
+      for (int d = -K; d <= K; ++d)
+        if (d != 0) v = fma_t(coef(K, K + d), buf[(rot + K + d) % NB][q], v);
+      acc[q] = v;
+    }
+  } else {
+    star_row_colchain<T, Q, K, NB>(buf, rot, coef, acc);
   }
 }
 
