@@ -542,8 +542,9 @@ def e2e_run(args, slab, st, world, rank, tb, ref_result):
             same = bool(torch.equal(chk, ref_result))
             del chk
             torch.cuda.empty_cache()
+        steps1 = min(steps, 4)  # the one-call-per-step number is a side figure
         t0 = time.perf_counter()
-        for _ in range(steps):
+        for _ in range(steps1):
             single()
         dt1 = time.perf_counter() - t0
 
@@ -567,8 +568,9 @@ def e2e_run(args, slab, st, world, rank, tb, ref_result):
                 "api": ("ssam_b200_stencil_batch (C ABI, pinned host grids, copies of "
                         "neighbouring steps overlapped with each step's sweeps)"),
                 "bit_identical_to_device_run": same_b,
-                "single_call": {"value": round(cells / dt1 / 1e9, 3), "unit": "GCells/s",
-                                "ms_per_step": round(dt1 / steps * 1e3, 3),
+                "single_call": {"value": round(cells / steps * steps1 / dt1 / 1e9, 3),
+                                "unit": "GCells/s", "steps": steps1,
+                                "ms_per_step": round(dt1 / steps1 * 1e3, 3),
                                 "api": "ssam_b200_stencil3d (C ABI, one synchronous call per step)",
                                 "bit_identical_to_device_run": same}}
 
@@ -766,7 +768,7 @@ def main():
     ap.add_argument("--halo", choices=["nccl", "peer"], default="nccl",
                     help="N > 1 halo transport: NCCL send/recv, or the sweep kernel's own "
                          "stores into the neighbours' buffers (CUDA IPC / NVLink P2P)")
-    ap.add_argument("--e2e-steps", type=int, default=12)
+    ap.add_argument("--e2e-steps", type=int, default=24)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-suite", action="store_true")
