@@ -154,6 +154,12 @@ cudaError_t multi_stencil(const T* h_in, T* h_out, int nx, int ny, int nz, const
                              cudaMemcpyHostToDevice, s.cs));
     SSAM_TRY(cudaMemcpyAsync(s.buf[1], s.buf[0], bytes, cudaMemcpyDeviceToDevice, s.cs));
   }
+  // Every slab's buffers are initialised before any neighbour's halo copy
+  // (on that neighbour's copy stream) may write into their ghost planes.
+  for (auto& s : sl) {
+    SSAM_TRY(cudaSetDevice(s.dev));
+    SSAM_TRY(cudaStreamSynchronize(s.cs));
+  }
 
   // Is a fused launch of this depth compiled for the stencil / dtype /
   // alignment?  (An empty output range validates without launching.)

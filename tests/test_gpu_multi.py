@@ -92,3 +92,16 @@ def test_multi_large_slabs(cuda_lib):
     one = cuda_lib.stencil3d(g, st, None, 12)
     got, used = cuda_lib.stencil_multi(g, st, [0, 0, 0, 0], None, 12)
     assert used == 4 and np.array_equal(got, one)
+
+
+def test_multi_headline_size(cuda_lib):
+    """The headline grid (2048^2 x 512 f32, 2^31 cells) on 2 and 4 slabs, 12
+    sweeps, equal to the one-device call bit for bit: at this size the
+    buffers' initial device copies take milliseconds, so a halo copy ordered
+    only after the neighbour's boundary launch would race them."""
+    st = cuda_lib.convert_stencil(cuda_lib.make_benchmark_stencil("3d7pt"), np.float32)
+    g = cuda_lib.random_grid3d(2048, 2048, 512, 0, np.float32)
+    one = cuda_lib.stencil3d(g, st, None, 12)
+    for n in (2, 4):
+        got, used = cuda_lib.stencil_multi(g, st, [0] * n, None, 12)
+        assert used == n and np.array_equal(got, one), n
