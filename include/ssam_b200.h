@@ -158,7 +158,8 @@ int ssam_b200_stencil3d_multi(int dtype, const void* in, int nx, int ny, int nz,
 /* A batch of independent grids (same shape and stencil) through the engine
  * with the PCIe copies overlapped: grid k's host->device copy, sweeps and
  * device->host copy run on three streams while neighbouring grids are in
- * other stages, `depth` grids in flight (0: 2), each with two device
+ * other stages, `depth` grids in flight (0: 2; bench.py uses 3, which
+ * keeps both neighbours' copies under a step's sweeps), each with two device
  * buffers.  Results equal `count` calls of ssam_b200_stencil2d/3d (no
  * config checks, no counters); pinned host buffers give the overlap.  2D
  * stencils pass nz = 1.  Blocks until every result is on the host. */
