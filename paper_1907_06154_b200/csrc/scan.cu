@@ -7,37 +7,51 @@
 // (oracle::scan_naive, oracle.hpp:118-127) -- exact for int64, the only type
 // its tests scan.
 //
-// B200 shape: reduce-then-scan over 32 KiB tiles (256 threads x rows of 4
-// elements per lane).
-//   1. scan_reduce_kernel: one CTA per tile sums it (read n).
-//   2. scan_carry_kernel: one CTA turns the tile sums into exclusive tile
-//      prefixes (32 serial sums per thread, one block ladder per 32 K tiles).
-//   3. scan_tile_kernel: one CTA per tile scans it from its prefix (read n,
-//      write n).
-// Within a tile every warp owns rows of 32 x 4 elements (coalesced 512-byte /
-// 1 KiB loads and stores); per row each lane scans its 4 elements serially and the
-// 32 lane totals run the same Kogge-Stone shfl_up ladder the reference
-// simulates (5 shuffles), warp totals one more ladder.  A single-pass
-// decoupled look-back (measured here at 2.0-2.5 TB/s on B200: the
-// inclusive-prefix chain across ~600 co-resident tiles, not HBM, bound it)
-// would also make floating-point results depend on timing; this order is
-// fixed, so every run is bit-identical.  Traffic is 3 x n element moves
-// against the 2 x n minimum.
+// B200 shape: an L2-chunked reduce-then-scan over 32 KiB tiles (256 threads x
+// rows of 4 elements per lane), one launch ("step") per chunk of kScanChunk
+// tiles (16 MiB of input).  Step c scans chunk c -- reduced by step c-1, so
+// its second read hits L2 -- and reduces chunk c+1.  HBM traffic is 2 x n
+// element moves (a 3-pass reduce/carry/scan moves 3 x n).
+//   * reduce blocks sum a tile of chunk c+1 into sums[] (input loads marked
+//     L2 evict_last: they are read again next step);
+//   * scan blocks scan their tile in registers, then form its exclusive
+//     prefix themselves: carry[c] + the chunk's earlier tile sums, in a fixed
+//     thread / tree order; block 0 also writes carry[c+1] = carry[c] +
+//     total(c).  Their loads and stores are marked evict_first.
+// Steps 0.. are programmatic-dependent launches with the reduce blocks first:
+// those read only the input, so they start while step c-1 drains; the scan
+// blocks griddep_wait for it.  Within a tile every warp owns rows of 32 x 4
+// elements (coalesced 512-byte / 1 KiB loads and stores); per row each lane
+// scans its 4 elements serially and the 32 lane totals run the same
+// Kogge-Stone shfl_up ladder the reference simulates (5 shuffles).  Every
+// association is fixed, so every run is bit-identical (a decoupled look-back
+// would make floating-point results depend on timing).  A/B against the
+// 3-pass form, plain launches, ready flags and one persistent kernel:
+// profiles/r02/scan_chunk_ab.txt.
+#include <algorithm>
 #include <cstdint>
+#include <cstring>
 
 #include "common.cuh"
 #include "internal.hpp"
+#include "launch.cuh"
 
 namespace ssam_b200 {
 
 namespace {
 
 constexpr int kScanThreads = 256;
-constexpr int kCarryThreads = 1024;
+#ifndef SSAM_SCAN_CHUNK
+#define SSAM_SCAN_CHUNK 512
+#endif
+#ifndef SSAM_SCAN_HINTS
+#define SSAM_SCAN_HINTS 1
+#endif
+constexpr int kScanChunk = SSAM_SCAN_CHUNK;
 
 // Each lane owns VQ = 4 consecutive elements per row (one 16-byte load for
 // fp32, two for 64-bit types), so the 5-step shuffle ladder is paid per 4
-// elements.  64-bit at 2^28: 2 per lane 2917 GB/s, 4 per lane 3921 (fp64) /
+// elements.  64-bit at 2^28 (3-pass form): 2 per lane 2917 GB/s, 4 per lane 3921 (fp64) /
 // 3885 (int64), 8 per lane 3799 / 3930.
 #ifndef SSAM_SCAN_VQ64
 #define SSAM_SCAN_VQ64 4
@@ -49,21 +63,64 @@ struct ScanTile {
   static constexpr int TILE = kScanThreads * ROWS * VQ;
 };
 
-// Loads warp `wid`'s rows of tile `tile` (zeros past n); returns whether the
-// tile is whole and 16-byte aligned (vector path).
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// 16-byte chunks with an L2 eviction-priority hint.
+template <class T, int Q>
+__device__ __forceinline__ void ldg_q_hint(const T* __restrict__ p, T (&out)[Q], uint64_t pol) {
+  constexpr int V = 16 / sizeof(T);
+#pragma unroll
+  for (int c = 0; c < Q / V; ++c) {
+    int4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p + c * V), "l"(pol));
+    T tmp[V];
+    memcpy(tmp, &r, 16);
+#pragma unroll
+    for (int q = 0; q < V; ++q) out[c * V + q] = tmp[q];
+  }
+}
+template <class T, int Q>
+__device__ __forceinline__ void st_q_hint(T* p, const T (&in)[Q], uint64_t pol) {
+  constexpr int V = 16 / sizeof(T);
+#pragma unroll
+  for (int c = 0; c < Q / V; ++c) {
+    int4 r;
+    memcpy(&r, in + c * V, 16);
+    asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p + c * V),
+                 "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "l"(pol)
+                 : "memory");
+  }
+}
+
+// Loads warp `wid`'s rows of tile `tile` (zeros past n) with L2 policy
+// `pol`; returns whether the tile is whole and 16-byte aligned (vector path).
 template <class T>
-__device__ __forceinline__ bool load_rows(const T* __restrict__ in, size_t n, int tile, int wid,
-                                          int lane, T (&v)[ScanTile<T>::ROWS][ScanTile<T>::VQ],
-                                          size_t& wbase) {
+__device__ __forceinline__ bool load_rows(const T* __restrict__ in, size_t n, size_t tile,
+                                          int wid, int lane,
+                                          T (&v)[ScanTile<T>::ROWS][ScanTile<T>::VQ],
+                                          size_t& wbase, uint64_t pol) {
   constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS, TILE = ScanTile<T>::TILE;
-  wbase = static_cast<size_t>(tile) * TILE + static_cast<size_t>(wid) * ROWS * 32 * VQ;
-  const bool full = static_cast<size_t>(tile + 1) * TILE <= n &&
-                    (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  wbase = tile * TILE + static_cast<size_t>(wid) * ROWS * 32 * VQ;
+  const bool full = (tile + 1) * TILE <= n && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
     const size_t at = wbase + static_cast<size_t>(r) * 32 * VQ + lane * VQ;
     if (full) {
+#if SSAM_SCAN_HINTS
+      ldg_q_hint<T, VQ>(in + at, v[r], pol);
+#else
       ldg_q<T, VQ>(in + at, v[r]);
+#endif
     } else {
 #pragma unroll
       for (int q = 0; q < VQ; ++q) v[r][q] = at + q < n ? in[at + q] : T(0);
@@ -72,99 +129,65 @@ __device__ __forceinline__ bool load_rows(const T* __restrict__ in, size_t n, in
   return full;
 }
 
+// Fixed-order sum of s[0 .. cnt) over the block (every thread gets it).
 template <class T>
-__global__ void __launch_bounds__(kScanThreads)
-    scan_reduce_kernel(const T* __restrict__ in, size_t n, T* __restrict__ tile_sum) {
-  constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS;
-  __shared__ T s_warp[kScanThreads / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  T v[ROWS][VQ];
-  size_t wbase;
-  load_rows<T>(in, n, blockIdx.x, wid, lane, v, wbase);
-  T x = T(0);
+__device__ __forceinline__ T block_sum_prefix(const T* __restrict__ s, int cnt, T* s_red,
+                                              int lane, int wid) {
+  constexpr int NW = kScanThreads / 32;
+  T acc = T(0);
+  for (int j = threadIdx.x; j < cnt; j += kScanThreads) acc += __ldcg(s + j);  // written this grid
 #pragma unroll
-  for (int r = 0; r < ROWS; ++r)
-#pragma unroll
-    for (int q = 0; q < VQ; ++q) x += v[r][q];
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(kFull, x, off);
-  if (lane == 0) s_warp[wid] = x;
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_down_sync(kFull, acc, off);
+  if (lane == 0) s_red[wid] = acc;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    T t = T(0);
+  T t = T(0);
 #pragma unroll
-    for (int w = 0; w < kScanThreads / 32; ++w) t += s_warp[w];
-    tile_sum[blockIdx.x] = t;
-  }
+  for (int w = 0; w < NW; ++w) t += s_red[w];
+  return t;
 }
 
-// Exclusive prefix of the tile sums: each of the 1024 threads scans
-// kCarryItems consecutive sums serially, one block-wide ladder joins the
-// thread totals, and a running carry links chunks of 1024 * kCarryItems sums
-// (16 items for 64-bit types keeps them in registers).
-template <class T>
-constexpr int carry_items() { return sizeof(T) == 4 ? 32 : 16; }
-
-template <class T>
-__global__ void __launch_bounds__(kCarryThreads)
-    scan_carry_kernel(const T* __restrict__ tile_sum, T* __restrict__ tile_prefix, int tiles) {
-  __shared__ T s_warp[kCarryThreads / 32];
-  __shared__ T s_carry;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_carry = T(0);
-  __syncthreads();
-  constexpr int kCarryItems = carry_items<T>();
-  for (long long base = 0; base < tiles; base += static_cast<long long>(kCarryThreads) * kCarryItems) {
-    const long long i0 = base + static_cast<long long>(threadIdx.x) * kCarryItems;
-    T v[kCarryItems];
-    T run = T(0);
-#pragma unroll
-    for (int k = 0; k < kCarryItems; ++k) {
-      v[k] = run;  // exclusive within the thread
-      run += i0 + k < tiles ? tile_sum[i0 + k] : T(0);
-    }
-    T t = run;
-#pragma unroll
-    for (int d = 1; d < 32; d *= 2) {
-      const T u = __shfl_up_sync(kFull, t, d);
-      if (lane >= d) t += u;
-    }
-    if (lane == 31) s_warp[wid] = t;
-    __syncthreads();
-    if (wid == 0) {
-      T w = s_warp[lane];
-#pragma unroll
-      for (int d = 1; d < 32; d *= 2) {
-        const T u = __shfl_up_sync(kFull, w, d);
-        if (lane >= d) w += u;
-      }
-      s_warp[lane] = w;
-    }
-    __syncthreads();
-    T ex = __shfl_up_sync(kFull, t, 1);
-    if (lane == 0) ex = T(0);
-    const T pre = s_carry + ((wid > 0 ? s_warp[wid - 1] : T(0)) + ex);
-#pragma unroll
-    for (int k = 0; k < kCarryItems; ++k)
-      if (i0 + k < tiles) tile_prefix[i0 + k] = pre + v[k];
-    __syncthreads();
-    if (threadIdx.x == kCarryThreads - 1) s_carry = pre + run;
-    __syncthreads();
-  }
-}
-
+// Step c (c = -1 .. chunks-1): blocks [0, rc) reduce chunk c+1, blocks
+// [rc, gridDim.x) scan chunk c.
 template <class T>
 __global__ void __launch_bounds__(kScanThreads)
-    scan_tile_kernel(const T* __restrict__ in, T* __restrict__ out, size_t n,
-                     const T* __restrict__ tile_prefix) {
+    scan_step_kernel(const T* __restrict__ in, T* __restrict__ out, size_t n,
+                     T* __restrict__ sums, T* __restrict__ carry, int c, int rc, int last_chunk) {
   constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS, NW = kScanThreads / 32;
   __shared__ T s_warp[NW];
+  __shared__ T s_red[NW];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   T v[ROWS][VQ];
   size_t wbase;
-  const bool full = load_rows<T>(in, n, blockIdx.x, wid, lane, v, wbase) &&
+  griddep_launch();  // step c+1's reduce blocks may fill SMs as this grid drains
+  if (static_cast<int>(blockIdx.x) < rc) {  // reduce a tile of chunk c+1
+    const int b = blockIdx.x;
+    const size_t tile = static_cast<size_t>(c + 1) * kScanChunk + b;
+    load_rows<T>(in, n, tile, wid, lane, v, wbase, l2_policy_last());
+    T x = T(0);
+#pragma unroll
+    for (int r = 0; r < ROWS; ++r)
+#pragma unroll
+      for (int q = 0; q < VQ; ++q) x += v[r][q];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) x += __shfl_down_sync(kFull, x, off);
+    if (lane == 0) s_warp[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      T t = T(0);
+#pragma unroll
+      for (int w = 0; w < NW; ++w) t += s_warp[w];
+      sums[tile] = t;
+      if (c < 0 && b == 0) carry[0] = T(0);
+    }
+    return;
+  }
+  // scan tile b of chunk c
+  const int b = blockIdx.x - rc, sc = gridDim.x - rc;
+  const size_t tile = static_cast<size_t>(c) * kScanChunk + b;
+  const uint64_t pol_first = l2_policy_first();
+  const bool full = load_rows<T>(in, n, tile, wid, lane, v, wbase, pol_first) &&
                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-  T carry = T(0);  // running total of the warp's earlier rows
+  T run = T(0);  // running total of the warp's earlier rows
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
 #pragma unroll
@@ -177,14 +200,22 @@ __global__ void __launch_bounds__(kScanThreads)
     }
     T ex = __shfl_up_sync(kFull, t, 1);  // exclusive lane prefix within the row
     if (lane == 0) ex = T(0);
-    ex += carry;
+    ex += run;
 #pragma unroll
     for (int q = 0; q < VQ; ++q) v[r][q] += ex;
-    carry += __shfl_sync(kFull, t, 31);
+    run += __shfl_sync(kFull, t, 31);
   }
-  if (lane == 0) s_warp[wid] = carry;
-  __syncthreads();
-  T add = tile_prefix[blockIdx.x];
+  if (lane == 0) s_warp[wid] = run;
+  griddep_wait();  // step c-1 (sums of chunk c, carry[c]) complete
+  const T* cs = sums + static_cast<size_t>(c) * kScanChunk;
+  const T cin = __ldcg(carry + c);
+  const T pre = cin + block_sum_prefix<T>(cs, b, s_red, lane, wid);  // syncs s_warp too
+  if (b == 0 && c < last_chunk) {
+    __syncthreads();  // s_red reuse
+    const T tot = block_sum_prefix<T>(cs, sc, s_red, lane, wid);
+    if (threadIdx.x == 0) carry[c + 1] = cin + tot;
+  }
+  T add = pre;
   for (int w = 0; w < wid; ++w) add += s_warp[w];
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
@@ -192,7 +223,11 @@ __global__ void __launch_bounds__(kScanThreads)
 #pragma unroll
     for (int q = 0; q < VQ; ++q) v[r][q] += add;
     if (full) {
+#if SSAM_SCAN_HINTS
+      st_q_hint<T, VQ>(out + at, v[r], pol_first);
+#else
       st_q<T, VQ>(out + at, v[r]);
+#endif
     } else {
 #pragma unroll
       for (int q = 0; q < VQ; ++q)
@@ -207,16 +242,29 @@ cudaError_t scan_impl(const T* d_in, T* d_out, size_t n, cudaStream_t s) {
   constexpr size_t TILE = ScanTile<T>::TILE;
   const size_t tiles = (n + TILE - 1) / TILE;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-  T* scratch = nullptr;  // tile sums, then tile prefixes (stream-ordered pool)
-  cudaError_t e = engine_alloc(reinterpret_cast<void**>(&scratch), 2 * tiles * sizeof(T), s);
+  const size_t chunks = (tiles + kScanChunk - 1) / kScanChunk;
+  T* scratch = nullptr;  // tile sums, then the chunk carries (stream-ordered pool)
+  cudaError_t e = engine_alloc(reinterpret_cast<void**>(&scratch),
+                               (tiles + chunks) * sizeof(T), s);
   if (e != cudaSuccess) return e;
-  const unsigned g = static_cast<unsigned>(tiles);
-  scan_reduce_kernel<T><<<g, kScanThreads, 0, s>>>(d_in, n, scratch);
-  scan_carry_kernel<T><<<1, kCarryThreads, 0, s>>>(scratch, scratch + tiles,
-                                                    static_cast<int>(tiles));
-  scan_tile_kernel<T><<<g, kScanThreads, 0, s>>>(d_in, d_out, n, scratch + tiles);
-  for (int k = 0; k < 3; ++k) note_launch();
-  e = cudaGetLastError();
+  T* carry = scratch + tiles;
+  const int last = static_cast<int>(chunks) - 1;
+  auto count = [&](long long c) -> unsigned {
+    if (c < 0 || c > last) return 0u;
+    return static_cast<unsigned>(std::min<size_t>(kScanChunk, tiles - c * kScanChunk));
+  };
+  for (int c = -1; c <= last && e == cudaSuccess; ++c) {
+    const unsigned sc = count(c), rc = count(c + 1);
+    if (c < 0) {  // an ordinary launch: orders the chain after d_in's producer
+      scan_step_kernel<T><<<rc, kScanThreads, 0, s>>>(d_in, d_out, n, scratch, carry, c,
+                                                       static_cast<int>(rc), last);
+    } else {
+      e = launch_pdl(scan_step_kernel<T>, dim3(sc + rc), dim3(kScanThreads), 0, s, d_in, d_out,
+                     n, scratch, carry, c, static_cast<int>(rc), last);
+    }
+    note_launch();
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
   return e;
 }

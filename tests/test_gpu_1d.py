@@ -99,7 +99,7 @@ def test_scan_criterion3_property(cuda_lib, orc):
 
 
 def test_scan_large_multi_tile(cuda_lib, orc):
-    """Many look-back tiles: 2^24 + 32 elements (int64 exact, f64 / f32 within tolerance)."""
+    """Many tiles and L2 chunks: 2^24 + 32 elements (int64 exact, f64 / f32 within tolerance)."""
     n = (1 << 24) + 32
     v = np.random.default_rng(3).integers(-1 << 20, 1 << 20, n).astype(np.int64)
     assert np.array_equal(cuda_lib.scan(v), orc.scan(v))
@@ -116,7 +116,7 @@ def test_scan_large_multi_tile(cuda_lib, orc):
 
 
 def test_scan_deterministic(cuda_lib, orc):
-    """One-pass scan with the canonical carry tree (scan.cu): repeated runs are
+    """Chunked scan with fixed-order tile prefixes (scan.cu): repeated runs are
     bit-identical for floating point too, whatever the tile timing."""
     n = (1 << 22) + 96
     for dt in (np.float32, np.float64):
@@ -124,3 +124,20 @@ def test_scan_deterministic(cuda_lib, orc):
         first = cuda_lib.scan(x)
         for _ in range(4):
             assert np.array_equal(cuda_lib.scan(x), first)
+
+
+def test_scan_chunk_boundaries(cuda_lib, orc):
+    """Lengths around the L2-chunk edges of scan.cu (512 tiles of 4096 int64 /
+    8192 fp32 elements): under one chunk, exactly one, a lane row over, two
+    chunks less a row, ragged last tiles (lengths are lane_count multiples).  int64 exact; fp32 against the
+    float64 prefix with the running-max scale."""
+    rng = np.random.default_rng(21)
+    for tiles, extra in ((511, 0), (512, 0), (512, 32), (513, -64), (1024, -32), (1025, 96)):
+        n = tiles * 4096 + extra
+        v = rng.integers(-1 << 30, 1 << 30, n).astype(np.int64)
+        assert np.array_equal(cuda_lib.scan(v), orc.scan(v)), (tiles, extra)
+    for tiles, extra in ((512, 0), (513, 160)):
+        x = orc.random_grid(tiles * 8192 + extra, np.float32, 5)
+        exact = np.cumsum(x.astype(np.float64))
+        scale = np.maximum(1.0, np.maximum.accumulate(np.abs(exact)))
+        assert float(np.max(np.abs(cuda_lib.scan(x) - exact) / scale)) <= 1e-5, tiles

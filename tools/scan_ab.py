@@ -17,6 +17,11 @@ for dt in (torch.float32, torch.float64):
     e.record(); torch.cuda.synchronize()
     ms = s.elapsed_time(e) / 5
     out.append(f"{str(dt)[6:]} {ms:.3f} ms {2*n*x.element_size()/ms/1e6:.0f} GB/s")
+xi = torch.randint(-1000, 1000, (n + 12345,), dtype=torch.int64, device="cuda"); yi = torch.empty_like(xi)
+dev.scan(xi, yi); out.append("int64 exact=" + str(bool(torch.equal(yi, torch.cumsum(xi, 0)))))
+xf = torch.empty(n + 777, dtype=torch.float64, device="cuda"); dev.fill_random(xf, 1); yf = torch.empty_like(xf)
+dev.scan(xf, yf); ref = torch.cumsum(xf, 0)
+out.append("f64 max_abs=%.2e" % (yf - ref).abs().max().item())
 print(" | ".join(out))
 '''
 for rep in range(2):
