@@ -8,8 +8,8 @@
 // its tests scan.
 //
 // B200 shape: an L2-chunked reduce-then-scan over 32 KiB tiles (256 threads x
-// rows of 4 elements per lane), one launch ("step") per chunk of kScanChunk
-// tiles (16 MiB of input).  Step c scans chunk c -- reduced by step c-1, so
+// rows of 4 elements per lane), one launch ("step") per chunk of CHUNK tiles
+// (12 MiB of fp32 / 16 MiB of 64-bit input).  Step c scans chunk c -- reduced by step c-1, so
 // its second read hits L2 -- and reduces chunk c+1.  HBM traffic is 2 x n
 // element moves (a 3-pass reduce/carry/scan moves 3 x n).
 //   * reduce blocks sum a tile of chunk c+1 into sums[] (input loads marked
@@ -41,13 +41,17 @@ namespace ssam_b200 {
 namespace {
 
 constexpr int kScanThreads = 256;
-#ifndef SSAM_SCAN_CHUNK
-#define SSAM_SCAN_CHUNK 512
+// Tiles per L2 chunk (profiles/r02/scan_chunk_ab.txt: fp32 296..1024 ->
+// 0.494..0.431 ms at 2^28 with the minimum 0.403 at 384; fp64 best at 512-592).
+#ifndef SSAM_SCAN_CHUNK32
+#define SSAM_SCAN_CHUNK32 384
+#endif
+#ifndef SSAM_SCAN_CHUNK64
+#define SSAM_SCAN_CHUNK64 512
 #endif
 #ifndef SSAM_SCAN_HINTS
 #define SSAM_SCAN_HINTS 1
 #endif
-constexpr int kScanChunk = SSAM_SCAN_CHUNK;
 
 // Each lane owns VQ = 4 consecutive elements per row (one 16-byte load for
 // fp32, two for 64-bit types), so the 5-step shuffle ladder is paid per 4
@@ -61,6 +65,7 @@ struct ScanTile {
   static constexpr int VQ = sizeof(T) == 4 ? 4 : SSAM_SCAN_VQ64;
   static constexpr int ROWS = sizeof(T) == 4 ? 8 : 16 / VQ;  // 32 KiB tiles
   static constexpr int TILE = kScanThreads * ROWS * VQ;
+  static constexpr int CHUNK = sizeof(T) == 4 ? SSAM_SCAN_CHUNK32 : SSAM_SCAN_CHUNK64;
 };
 
 __device__ __forceinline__ uint64_t l2_policy_last() {
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(kScanThreads)
   griddep_launch();  // step c+1's reduce blocks may fill SMs as this grid drains
   if (static_cast<int>(blockIdx.x) < rc) {  // reduce a tile of chunk c+1
     const int b = blockIdx.x;
-    const size_t tile = static_cast<size_t>(c + 1) * kScanChunk + b;
+    const size_t tile = static_cast<size_t>(c + 1) * ScanTile<T>::CHUNK + b;
     load_rows<T>(in, n, tile, wid, lane, v, wbase, l2_policy_last());
     T x = T(0);
 #pragma unroll
@@ -183,7 +188,7 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   // scan tile b of chunk c
   const int b = blockIdx.x - rc, sc = gridDim.x - rc;
-  const size_t tile = static_cast<size_t>(c) * kScanChunk + b;
+  const size_t tile = static_cast<size_t>(c) * ScanTile<T>::CHUNK + b;
   const uint64_t pol_first = l2_policy_first();
   const bool full = load_rows<T>(in, n, tile, wid, lane, v, wbase, pol_first) &&
                     (reinterpret_cast<uintptr_t>(out) & 15) == 0;
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(kScanThreads)
   }
   if (lane == 0) s_warp[wid] = run;
   griddep_wait();  // step c-1 (sums of chunk c, carry[c]) complete
-  const T* cs = sums + static_cast<size_t>(c) * kScanChunk;
+  const T* cs = sums + static_cast<size_t>(c) * ScanTile<T>::CHUNK;
   const T cin = __ldcg(carry + c);
   const T pre = cin + block_sum_prefix<T>(cs, b, s_red, lane, wid);  // syncs s_warp too
   if (b == 0 && c < last_chunk) {
@@ -242,16 +247,17 @@ cudaError_t scan_impl(const T* d_in, T* d_out, size_t n, cudaStream_t s) {
   constexpr size_t TILE = ScanTile<T>::TILE;
   const size_t tiles = (n + TILE - 1) / TILE;
   if (tiles > 0x7fffffff) return cudaErrorInvalidValue;
-  const size_t chunks = (tiles + kScanChunk - 1) / kScanChunk;
+  const size_t chunks = (tiles + ScanTile<T>::CHUNK - 1) / ScanTile<T>::CHUNK;
   T* scratch = nullptr;  // tile sums, then the chunk carries (stream-ordered pool)
   cudaError_t e = engine_alloc(reinterpret_cast<void**>(&scratch),
                                (tiles + chunks) * sizeof(T), s);
   if (e != cudaSuccess) return e;
   T* carry = scratch + tiles;
   const int last = static_cast<int>(chunks) - 1;
+  constexpr size_t CH = ScanTile<T>::CHUNK;
   auto count = [&](long long c) -> unsigned {
     if (c < 0 || c > last) return 0u;
-    return static_cast<unsigned>(std::min<size_t>(kScanChunk, tiles - c * kScanChunk));
+    return static_cast<unsigned>(std::min<size_t>(CH, tiles - c * CH));
   };
   for (int c = -1; c <= last && e == cudaSuccess; ++c) {
     const unsigned sc = count(c), rc = count(c + 1);

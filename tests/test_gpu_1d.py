@@ -128,7 +128,7 @@ def test_scan_deterministic(cuda_lib, orc):
 
 def test_scan_chunk_boundaries(cuda_lib, orc):
     """Lengths around the L2-chunk edges of scan.cu (512 tiles of 4096 int64 /
-    8192 fp32 elements): under one chunk, exactly one, a lane row over, two
+    384 tiles of 8192 fp32 elements): under one chunk, exactly one, a lane row over, two
     chunks less a row, ragged last tiles (lengths are lane_count multiples).  int64 exact; fp32 against the
     float64 prefix with the running-max scale."""
     rng = np.random.default_rng(21)
@@ -136,7 +136,7 @@ def test_scan_chunk_boundaries(cuda_lib, orc):
         n = tiles * 4096 + extra
         v = rng.integers(-1 << 30, 1 << 30, n).astype(np.int64)
         assert np.array_equal(cuda_lib.scan(v), orc.scan(v)), (tiles, extra)
-    for tiles, extra in ((512, 0), (513, 160)):
+    for tiles, extra in ((384, 0), (385, 160), (768, -32)):
         x = orc.random_grid(tiles * 8192 + extra, np.float32, 5)
         exact = np.cumsum(x.astype(np.float64))
         scale = np.maximum(1.0, np.maximum.accumulate(np.abs(exact)))
