@@ -8,8 +8,8 @@
 // its tests scan.
 //
 // B200 shape: an L2-chunked reduce-then-scan over 32 KiB tiles (256 threads x
-// rows of 4 elements per lane), one launch ("step") per chunk of CHUNK tiles
-// (12 MiB of fp32 / 16 MiB of 64-bit input).  Step c scans chunk c -- reduced by step c-1, so
+// rows of 4 elements per lane), one launch ("step") per chunk of CHUNK = 384
+// tiles (12 MiB of input).  Step c scans chunk c -- reduced by step c-1, so
 // its second read hits L2 -- and reduces chunk c+1.  HBM traffic is 2 x n
 // element moves (a 3-pass reduce/carry/scan moves 3 x n).
 //   * reduce blocks sum a tile of chunk c+1 into sums[] (input loads marked
@@ -41,31 +41,37 @@ namespace ssam_b200 {
 namespace {
 
 constexpr int kScanThreads = 256;
-// Tiles per L2 chunk (profiles/r02/scan_chunk_ab.txt: fp32 296..1024 ->
-// 0.494..0.431 ms at 2^28 with the minimum 0.403 at 384; fp64 best at 512-592).
-#ifndef SSAM_SCAN_CHUNK32
-#define SSAM_SCAN_CHUNK32 384
+// Tiles per L2 chunk, 12 MiB (profiles/r02/scan_chunk_ab.txt: 296..2048 tiles
+// span 0.494..0.403 ms for fp32 at 2^28, the minimum at 384; fp64 with 256-bit
+// accesses 0.813 ms at 384, 0.865 at 512).
+#ifndef SSAM_SCAN_CHUNK
+#define SSAM_SCAN_CHUNK 384
 #endif
-#ifndef SSAM_SCAN_CHUNK64
-#define SSAM_SCAN_CHUNK64 512
+#ifndef SSAM_SCAN_V256
+#define SSAM_SCAN_V256 1
 #endif
 #ifndef SSAM_SCAN_HINTS
 #define SSAM_SCAN_HINTS 1
 #endif
 
-// Each lane owns VQ = 4 consecutive elements per row (one 16-byte load for
-// fp32, two for 64-bit types), so the 5-step shuffle ladder is paid per 4
-// elements.  64-bit at 2^28 (3-pass form): 2 per lane 2917 GB/s, 4 per lane 3921 (fp64) /
-// 3885 (int64), 8 per lane 3799 / 3930.
+// Each lane owns VQ = 4 consecutive elements per row (one 16-byte access for
+// fp32, one 256-bit access for 64-bit types), so the 5-step shuffle ladder is
+// paid per 4 elements.  Measured: 64-bit VQ 2 / 8 lose (3-pass form and the
+// chunked one), fp32 VQ 8 (256-bit) is within 1%.
+#ifndef SSAM_SCAN_VQ32
+#define SSAM_SCAN_VQ32 4
+#endif
 #ifndef SSAM_SCAN_VQ64
 #define SSAM_SCAN_VQ64 4
 #endif
 template <class T>
 struct ScanTile {
-  static constexpr int VQ = sizeof(T) == 4 ? 4 : SSAM_SCAN_VQ64;
-  static constexpr int ROWS = sizeof(T) == 4 ? 8 : 16 / VQ;  // 32 KiB tiles
+  static constexpr int VQ = sizeof(T) == 4 ? SSAM_SCAN_VQ32 : SSAM_SCAN_VQ64;
+  static constexpr int ROWS = 128 / (VQ * sizeof(T));  // 32 KiB tiles
   static constexpr int TILE = kScanThreads * ROWS * VQ;
-  static constexpr int CHUNK = sizeof(T) == 4 ? SSAM_SCAN_CHUNK32 : SSAM_SCAN_CHUNK64;
+  static constexpr int CHUNK = SSAM_SCAN_CHUNK;
+  // base-address alignment the vector path needs (256-bit for 64-bit types)
+  static constexpr uintptr_t ALIGN = (sizeof(T) * VQ == 32 && SSAM_SCAN_V256) ? 31 : 15;
 };
 
 __device__ __forceinline__ uint64_t l2_policy_last() {
@@ -78,32 +84,51 @@ __device__ __forceinline__ uint64_t l2_policy_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-// 16-byte chunks with an L2 eviction-priority hint.
+// A lane's Q elements with an L2 eviction-priority hint: one 256-bit access
+// when they span 32 bytes (64-bit types, Q = 4: a warp row is one fully
+// coalesced 1 KiB request instead of two half-used 16-byte ones), else
+// 16-byte chunks.
 template <class T, int Q>
 __device__ __forceinline__ void ldg_q_hint(const T* __restrict__ p, T (&out)[Q], uint64_t pol) {
-  constexpr int V = 16 / sizeof(T);
+  if constexpr (sizeof(T) * Q == 32 && SSAM_SCAN_V256) {
+    unsigned long long r[4];
+    asm volatile("ld.global.nc.L2::cache_hint.v4.b64 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=l"(r[0]), "=l"(r[1]), "=l"(r[2]), "=l"(r[3])
+                 : "l"(p), "l"(pol));
+    memcpy(out, r, 32);
+  } else {
+    constexpr int V = 16 / sizeof(T);
 #pragma unroll
-  for (int c = 0; c < Q / V; ++c) {
-    int4 r;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p + c * V), "l"(pol));
-    T tmp[V];
-    memcpy(tmp, &r, 16);
+    for (int c = 0; c < Q / V; ++c) {
+      int4 r;
+      asm volatile("ld.global.nc.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;"
+                   : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                   : "l"(p + c * V), "l"(pol));
+      T tmp[V];
+      memcpy(tmp, &r, 16);
 #pragma unroll
-    for (int q = 0; q < V; ++q) out[c * V + q] = tmp[q];
+      for (int q = 0; q < V; ++q) out[c * V + q] = tmp[q];
+    }
   }
 }
 template <class T, int Q>
 __device__ __forceinline__ void st_q_hint(T* p, const T (&in)[Q], uint64_t pol) {
-  constexpr int V = 16 / sizeof(T);
-#pragma unroll
-  for (int c = 0; c < Q / V; ++c) {
-    int4 r;
-    memcpy(&r, in + c * V, 16);
-    asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p + c * V),
-                 "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "l"(pol)
+  if constexpr (sizeof(T) * Q == 32 && SSAM_SCAN_V256) {
+    unsigned long long r[4];
+    memcpy(r, in, 32);
+    asm volatile("st.global.L2::cache_hint.v4.b64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "l"(r[0]),
+                 "l"(r[1]), "l"(r[2]), "l"(r[3]), "l"(pol)
                  : "memory");
+  } else {
+    constexpr int V = 16 / sizeof(T);
+#pragma unroll
+    for (int c = 0; c < Q / V; ++c) {
+      int4 r;
+      memcpy(&r, in + c * V, 16);
+      asm volatile("st.global.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p + c * V),
+                   "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "l"(pol)
+                   : "memory");
+    }
   }
 }
 
@@ -116,7 +141,8 @@ __device__ __forceinline__ bool load_rows(const T* __restrict__ in, size_t n, si
                                           size_t& wbase, uint64_t pol) {
   constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS, TILE = ScanTile<T>::TILE;
   wbase = tile * TILE + static_cast<size_t>(wid) * ROWS * 32 * VQ;
-  const bool full = (tile + 1) * TILE <= n && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+  const bool full =
+      (tile + 1) * TILE <= n && (reinterpret_cast<uintptr_t>(in) & ScanTile<T>::ALIGN) == 0;
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {
     const size_t at = wbase + static_cast<size_t>(r) * 32 * VQ + lane * VQ;
@@ -191,7 +217,7 @@ __global__ void __launch_bounds__(kScanThreads)
   const size_t tile = static_cast<size_t>(c) * ScanTile<T>::CHUNK + b;
   const uint64_t pol_first = l2_policy_first();
   const bool full = load_rows<T>(in, n, tile, wid, lane, v, wbase, pol_first) &&
-                    (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+                    (reinterpret_cast<uintptr_t>(out) & ScanTile<T>::ALIGN) == 0;
   T run = T(0);  // running total of the warp's earlier rows
 #pragma unroll
   for (int r = 0; r < ROWS; ++r) {

@@ -127,12 +127,12 @@ def test_scan_deterministic(cuda_lib, orc):
 
 
 def test_scan_chunk_boundaries(cuda_lib, orc):
-    """Lengths around the L2-chunk edges of scan.cu (512 tiles of 4096 int64 /
-    384 tiles of 8192 fp32 elements): under one chunk, exactly one, a lane row over, two
+    """Lengths around the L2-chunk edges of scan.cu (384 tiles of 4096 int64 /
+    8192 fp32 elements): under one chunk, exactly one, a lane row over, two
     chunks less a row, ragged last tiles (lengths are lane_count multiples).  int64 exact; fp32 against the
     float64 prefix with the running-max scale."""
     rng = np.random.default_rng(21)
-    for tiles, extra in ((511, 0), (512, 0), (512, 32), (513, -64), (1024, -32), (1025, 96)):
+    for tiles, extra in ((383, 0), (384, 0), (384, 32), (385, -64), (768, -32), (769, 96)):
         n = tiles * 4096 + extra
         v = rng.integers(-1 << 30, 1 << 30, n).astype(np.int64)
         assert np.array_equal(cuda_lib.scan(v), orc.scan(v)), (tiles, extra)
@@ -141,3 +141,30 @@ def test_scan_chunk_boundaries(cuda_lib, orc):
         exact = np.cumsum(x.astype(np.float64))
         scale = np.maximum(1.0, np.maximum.accumulate(np.abs(exact)))
         assert float(np.max(np.abs(cuda_lib.scan(x) - exact) / scale)) <= 1e-5, tiles
+
+
+def test_scan_device_unaligned_views():
+    """Device scan on views whose base is off the 32-byte (64-bit) / 16-byte
+    (fp32) vector alignment: the tiles take the scalar path, same results."""
+    import torch
+    from paper_1907_06154_b200 import device as dev
+    n = 384 * 4096 + 4096 + 160
+    g = torch.Generator().manual_seed(5)
+    base = torch.randint(-1 << 30, 1 << 30, (n + 8,), generator=g, dtype=torch.int64).cuda()
+    for off_in, off_out in ((1, 3), (2, 0), (0, 2), (4, 4)):
+        x = base[off_in:off_in + n]
+        y = torch.zeros(n + 8, dtype=torch.int64, device="cuda")[off_out:off_out + n]
+        dev.scan(x, y)
+        assert torch.equal(y, torch.cumsum(x, 0)), (off_in, off_out)
+    xf = torch.rand(n + 8, generator=g, dtype=torch.float64).cuda()
+    for off in (1, 2):
+        x = xf[off:off + n]
+        y = torch.empty(n + 8, dtype=torch.float64, device="cuda")[off:off + n]
+        dev.scan(x, y)
+        ref = torch.cumsum(x, 0)
+        assert float(((y - ref).abs() / ref.abs().clamp_min(1)).max()) <= 1e-12, off
+    x32 = torch.rand(n + 8, generator=g, dtype=torch.float32).cuda()[1:n + 1]
+    y32 = torch.empty(n + 8, dtype=torch.float32, device="cuda")[1:n + 1]
+    dev.scan(x32, y32)
+    ref = torch.cumsum(x32.double(), 0)
+    assert float(((y32.double() - ref).abs() / ref.abs().clamp_min(1)).max()) <= 1e-5

@@ -37,7 +37,7 @@ dev.conv1d(x, y, np.ones(9, np.float32)); dev.scan(x, y)
 for dt in (torch.float64, torch.int64):
     x = grid(70001, dt); y = torch.empty_like(x)
     dev.scan(x, y)
-# the chunked scan across several L2 chunks (384 / 512 tiles) and a ragged tail
+# the chunked scan across several L2 chunks (384 tiles) and a ragged tail
 for dt, per in ((torch.float32, 8192), (torch.int64, 4096)):
     x = grid(1025 * per + 517, dt)
     y = torch.empty_like(x)
