@@ -4,7 +4,7 @@
 // cache row: M broadcast-weight MAD stages with a one-lane shift between
 // them.  A signal is therefore a one-row grid for the 2D SSAM engine
 // (engine2d.cuh): a warp walks CH consecutive windows of 32 x Q samples
-// (128-bit loads), runs the bidirectional shuffle chain over the M taps and
+// (256-bit loads), runs the bidirectional shuffle chain over the M taps and
 // stores its own Q outputs per window; consecutive windows overlap by the
 // M-1 halo samples.
 // The weights are flipped exactly as for conv2d (w[s] -> coef[M-1-s]), so
@@ -16,8 +16,32 @@ namespace ssam_b200 {
 
 namespace {
 
+// Samples per lane: 32 bytes (one 256-bit load, sm_100).  At 2^28, m = 9:
+// fp32 Q 4 -> 8 0.375 -> 0.336 ms, fp64 Q 2 -> 4 0.811 -> 0.661 ms; m = 32
+// 0.80 -> 0.51 / 2.36 -> 1.09 ms -- fewer shuffles per output and a smaller
+// window overlap; bit-identical (profiles/r02/conv1d_q_ab.txt).
+#ifndef SSAM_C1D_Q32
+#define SSAM_C1D_Q32 8
+#endif
+#ifndef SSAM_C1D_Q64
+#define SSAM_C1D_Q64 4
+#endif
+template <class T>
+constexpr int c1d_q() { return sizeof(T) == 4 ? SSAM_C1D_Q32 : SSAM_C1D_Q64; }
+
+// A lane's Q samples as one 256-bit load when they span 32 bytes.
+template <class T, int Q>
+__device__ __forceinline__ void ldg_q256(const T* __restrict__ p, T (&out)[Q]) {
+  static_assert(sizeof(T) * Q == 32, "256-bit vectors only");
+  unsigned long long r[4];
+  asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+               : "=l"(r[0]), "=l"(r[1]), "=l"(r[2]), "=l"(r[3])
+               : "l"(p));
+  memcpy(out, r, 32);
+}
+
 // One warp per run of CH consecutive chunks of V outputs: every chunk is one
-// 32 x Q window (128-bit loads; the M-1 overlap with the previous chunk hits
+// 32 x Q window (256-bit loads; the M-1 overlap with the previous chunk hits
 // L1), the bidirectional chain of engine2d.cuh, and the lane's own Q stores.
 template <class T, int Q, int CH, int CAP>
 __global__ void __launch_bounds__(128) conv1d_kernel(const __grid_constant__ Ssam2DParams<T, CAP> p) {
@@ -32,7 +56,14 @@ __global__ void __launch_bounds__(128) conv1d_kernel(const __grid_constant__ Ssa
     const int col0 = x_out0 - p.A + Q * lane;
     const bool fast = p.vec_ok && x_out0 - p.A >= 0 && x_out0 - p.A + 32 * Q <= p.W;
     T buf[1][Q];
-    load_row<T, Q>(p.in, p.W, 1, 0, col0, fast, p.bmode, buf[0]);
+    if constexpr (sizeof(T) * Q == 32) {
+      if (fast)
+        ldg_q256<T, Q>(p.in + col0, buf[0]);
+      else
+        load_row<T, Q>(p.in, p.W, 1, 0, col0, false, p.bmode, buf[0]);
+    } else {
+      load_row<T, Q>(p.in, p.W, 1, 0, col0, fast, p.bmode, buf[0]);
+    }
     T acc[Q];
     ssam_row<T, Q, 1, 0, DenseMask, 1, CAP>(buf, 0, p, acc);
     store_row<T, Q, CAP>(p, store_plan<T, Q, CAP>(p, x_out0, col0, p.vec_ok != 0), 0, acc);
@@ -44,7 +75,7 @@ cudaError_t conv1d_impl(const T* d_in, T* d_out, int len, const T* h_w, int m, i
                         cudaStream_t s) {
   if (len <= 0) return cudaSuccess;
   if (m < 1 || m > 32) return cudaErrorInvalidValue;
-  constexpr int Q = Lanes<T>::Q, CH = 8, CAP = 32;
+  constexpr int Q = c1d_q<T>(), CH = 8, CAP = 32;
   const std::vector<T> coef = conv_coef(h_w, m, 1);
   Ssam2DParams<T, CAP> p;
   std::memset(&p, 0, sizeof(p));
@@ -61,7 +92,9 @@ cudaError_t conv1d_impl(const T* d_in, T* d_out, int len, const T* h_w, int m, i
   p.y_begin = 0;
   p.y_end = 1;
   p.bmode = boundary ? kBndReplicate : kBndZero;
-  p.vec_ok = (len % Q == 0) && aligned16(d_in) && aligned16(d_out);
+  const uintptr_t amask = sizeof(T) * Q == 32 ? 31 : 15;  // 256-bit loads need 32 B
+  p.vec_ok = (len % Q == 0) && (reinterpret_cast<uintptr_t>(d_in) & amask) == 0 &&
+             aligned16(d_out);
   std::memcpy(p.coef, coef.data(), sizeof(T) * m);
   const long long warps = (p.nstrips + CH - 1) / CH;
   const unsigned blocks = static_cast<unsigned>((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);

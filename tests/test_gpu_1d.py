@@ -168,3 +168,26 @@ def test_scan_device_unaligned_views():
     dev.scan(x32, y32)
     ref = torch.cumsum(x32.double(), 0)
     assert float(((y32.double() - ref).abs() / ref.abs().clamp_min(1)).max()) <= 1e-5
+
+
+def test_conv1d_device_unaligned_views():
+    """conv1d on views off the 32-byte vector alignment (scalar loads) equals
+    the aligned run bit for bit, fp32 and fp64, zero and replicate edges."""
+    import torch
+    from paper_1907_06154_b200 import device as dev
+    n = 100000
+    g = torch.Generator().manual_seed(9)
+    for dt in (torch.float32, torch.float64):
+        base = torch.rand(n + 8, generator=g, dtype=dt).cuda()
+        for m in (3, 9, 32):
+            w = np.linspace(-1, 1, m)
+            for bnd in (0, 1):
+                ref_in = base[:n].clone()
+                ref = torch.empty_like(ref_in)
+                dev.conv1d(ref_in, ref, w, bnd)
+                for off in (1, 2, 3):
+                    x = base.clone()[off:off + n]
+                    x.copy_(base[:n])
+                    y = torch.empty(n + 8, dtype=dt, device="cuda")[off:off + n]
+                    dev.conv1d(x, y, w, bnd)
+                    assert torch.equal(y, ref), (dt, m, bnd, off)
