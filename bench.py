@@ -733,7 +733,7 @@ def kernel_suite(peak, sm_mhz):
             "ms": round(ms, 3), "tb": tbk,
             "note": f"cell-updates/s of one fused {tbk}-sweep launch (8 B/cell per launch)"}
     del a, bb
-    # 1D (kernels.hpp:390-447): conv1d 9 taps and the one-pass scan over 2^28 elements
+    # 1D (kernels.hpp:390-447): conv1d 9 taps and the chunked two-pass scan over 2^28 elements
     # (1 GiB fp32, far above L2), HBM-bound at 2 * sizeof(T) bytes per element.
     n1 = 1 << 28
     for dt, tdt, npdt, sz in (("f32", torch.float32, np.float32, 4),

@@ -322,7 +322,9 @@ int ssam_b200_check_scan(unsigned long long len, int lane_count);
 int ssam_b200_counters_conv1d(long long len, int m, const ssam_kernel_config* cfg,
                               ssam_op_counters* counters);
 int ssam_b200_counters_scan(unsigned long long len, int lane_count, ssam_op_counters* counters);
-/* Device-resident, stream-ordered: conv1d (m <= 32) and a one-pass scan. */
+/* Device-resident, stream-ordered: conv1d (m <= 32; d_in and d_out may not
+ * overlap) and the scan (an L2-chunked reduce-then-scan, one launch per
+ * 12 MiB of input; d_out == d_in scans in place). */
 int ssam_b200_conv1d_device(int dtype, const void* d_in, void* d_out, int len,
                             const void* h_weights, int m, int boundary, void* stream);
 int ssam_b200_scan_device(int dtype, const void* d_in, void* d_out, size_t len, void* stream);

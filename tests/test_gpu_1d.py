@@ -191,3 +191,21 @@ def test_conv1d_device_unaligned_views():
                     y = torch.empty(n + 8, dtype=dt, device="cuda")[off:off + n]
                     dev.conv1d(x, y, w, bnd)
                     assert torch.equal(y, ref), (dt, m, bnd, off)
+
+
+def test_scan_device_in_place():
+    """d_out == d_in (ssam_b200.h): every chunk's tiles are read before they
+    are written, int64 exact, fp32 equal to the out-of-place result."""
+    import torch
+    from paper_1907_06154_b200 import device as dev
+    n = 3 * 384 * 4096 + 4096 + 96
+    g = torch.Generator().manual_seed(13)
+    x = torch.randint(-1 << 30, 1 << 30, (n,), generator=g, dtype=torch.int64).cuda()
+    want = torch.cumsum(x, 0)
+    dev.scan(x, x)
+    assert torch.equal(x, want)
+    f = torch.rand(n, generator=g, dtype=torch.float32).cuda()
+    ref = torch.empty_like(f)
+    dev.scan(f, ref)
+    dev.scan(f, f)
+    assert torch.equal(f, ref)
