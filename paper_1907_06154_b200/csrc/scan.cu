@@ -179,8 +179,10 @@ __device__ __forceinline__ T block_sum_prefix(const T* __restrict__ s, int cnt, 
 
 // Step c (c = -1 .. chunks-1): blocks [0, rc) reduce chunk c+1, blocks
 // [rc, gridDim.x) scan chunk c.
+// 4 CTAs per SM (<= 64 registers): the step is latency-bound, and 93-108
+// registers (3 CTAs) cost 25-30%, 5 CTAs spill (profiles/r02/scan_chunk_ab.txt).
 template <class T>
-__global__ void __launch_bounds__(kScanThreads)
+__global__ void __launch_bounds__(kScanThreads, 4)
     scan_step_kernel(const T* __restrict__ in, T* __restrict__ out, size_t n,
                      T* __restrict__ sums, T* __restrict__ carry, int c, int rc, int last_chunk) {
   constexpr int VQ = ScanTile<T>::VQ, ROWS = ScanTile<T>::ROWS, NW = kScanThreads / 32;
