@@ -26,7 +26,8 @@
 // Kogge-Stone shfl_up ladder the reference simulates (5 shuffles).  Every
 // association is fixed, so every run is bit-identical (a decoupled look-back
 // would make floating-point results depend on timing).  A/B against the
-// 3-pass form, plain launches, ready flags and one persistent kernel:
+// 3-pass form, plain launches, ready flags, a bulk-copy step and one
+// persistent kernel:
 // profiles/r02/scan_chunk_ab.txt.
 #include <algorithm>
 #include <cstdint>
